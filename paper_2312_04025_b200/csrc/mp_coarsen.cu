@@ -1,0 +1,714 @@
+// mp_coarsen.cu — GCOF fusion-rule coarsening on the GPU (K1/K2), sm_100a.
+//
+// Reference: pkg/src/opplace/fusion.py:93-104 (_match_seqs), :117-130
+// (_combined_cost), :133-248 (_Coarsener), :271-304 (gcof).  Semantics and the
+// parallelisation argument are in DESIGN.md §5 and SURVEY.md App. B.
+//
+// Phases
+//  K1a (parallel)  degrees, CSR of successors sorted by (src, dst) with a radix
+//                  sort, Kahn levels (the validate_dag cycle check,
+//                  graph.py:267-288), rule trie, per-node trie state of its own
+//                  type sequence.
+//  K1b (ordered)   the reference DFS (fusion.py:281-303).  Which producer claims
+//                  a multi-input consumer, and whether a consumer had already
+//                  extended itself when absorbed, depend on the lexicographic DFS
+//                  order — a P-complete order in general — so this phase replays
+//                  the DFS exactly, on one GPU thread, over compact state.
+//                  No out/inn sets are kept: a group's quotient out-set is the
+//                  set of current groups of its tail member's input successors
+//                  (App. B: out(combine(a, b)) = out(b)), and the rule match is a
+//                  walk in the trie from the predecessor's state.  creates_cycle
+//                  is provably false inside gcof (fusion.py:155-167 is only
+//                  reached with out[cur] == {nxt}) and is not evaluated.
+//  K2  (parallel)  final_partition (fusion.py:195-219) one thread per group;
+//                  output ids by compaction in index order; member-order mem
+//                  sums and fused costs (overrides first, else the CPython
+//                  sum() of member times — Neumaier-compensated on >= 3.12);
+//                  quotient edges: radix sort of (gu, gv) keys + segmented
+//                  payload sum, which yields the reference's sorted edge list.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "mp_common.cuh"
+
+namespace {
+
+constexpr int kDead = -1;
+constexpr int kTagPlain = 0, kTagFused = 1, kTagBound = 2;
+
+int cset_err(mp_error *err, int code, int64_t a, int64_t b, const char *fmt, ...) {
+    if (err) {
+        err->code = code;
+        err->a = a;
+        err->b = b;
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CK(call)                                                                                       \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess)                                                                         \
+            return cset_err(err, MP_ERR_CUDA, static_cast<int64_t>(e_), 0, "%s: %s (%s:%d)", #call,   \
+                            cudaGetErrorString(e_), __FILE__, __LINE__);                               \
+    } while (0)
+
+// Rule trie: node 0 is the root.  Children are a singly linked list.
+struct Trie {
+    int *child;     // first child
+    int *sibling;   // next sibling
+    int *type;      // edge label into this node
+    int *flags;     // bit0 terminal (a full pattern), bit1 has children
+    int n;
+};
+
+__device__ __forceinline__ int trie_step(const Trie &t, int s, int ty) {
+    if (s < 0) return kDead;
+    for (int c = t.child[s]; c >= 0; c = t.sibling[c])
+        if (t.type[c] == ty) return c;
+    return kDead;
+}
+
+__global__ void k_build_trie(int R, const int *rule_beg, const int *rule_types, Trie t, int *n_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int n = 1;
+    t.child[0] = -1;
+    t.sibling[0] = -1;
+    t.type[0] = -1;
+    t.flags[0] = 0;
+    for (int r = 0; r < R; ++r) {
+        int s = 0;
+        for (int q = rule_beg[r]; q < rule_beg[r + 1]; ++q) {
+            const int ty = rule_types[q];
+            int c = t.child[s];
+            while (c >= 0 && t.type[c] != ty) c = t.sibling[c];
+            if (c < 0) {
+                c = n++;
+                t.child[c] = -1;
+                t.type[c] = ty;
+                t.flags[c] = 0;
+                t.sibling[c] = t.child[s];
+                t.child[s] = c;
+                t.flags[s] |= 2;
+            }
+            s = c;
+        }
+        t.flags[s] |= 1;
+    }
+    *n_out = n;
+}
+
+struct DfsState {
+    int *where;     // [V] current group of each input node
+    int *next;      // [V] next member in chain order (-1 = tail)
+    int *head;      // [V] by group id: first member
+    int *tail;      // [V] by group id: last member
+    int *state;     // [V] by group id: trie state of the group's type sequence
+    int *len;       // [V] by group id: sequence length (capped at Lmax+1)
+    int *seq;       // [V*Lmax] by group id: the sequence (valid when len <= Lmax)
+    int *tag;       // [V] by group id
+    unsigned char *visited;  // [V] by group id
+};
+
+// Initial per-node state: singleton groups with the node's own type sequence.
+__global__ void k_init_nodes(int V, int Lmax, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
+                             DfsState s) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        s.where[v] = v;
+        s.next[v] = -1;
+        s.head[v] = v;
+        s.tail[v] = v;
+        s.tag[v] = tag_in[v];
+        s.visited[v] = 0;
+        const int b = seq_beg[v], e = seq_beg[v + 1];
+        int st = 0;
+        for (int q = b; q < e; ++q) st = trie_step(t, st, seq_types[q]);
+        s.state[v] = st;
+        const int L = e - b;
+        s.len[v] = L <= Lmax ? L : Lmax + 1;
+        for (int q = 0; q < L && q < Lmax; ++q) s.seq[static_cast<size_t>(v) * Lmax + q] = seq_types[b + q];
+    }
+}
+
+__global__ void k_split_keys(int E, const unsigned long long *keys, int *dst, int *cnt) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[e];
+        dst[e] = static_cast<int>(k & 0xffffffffULL);
+        atomicAdd(&cnt[static_cast<int>(k >> 32)], 1);
+    }
+}
+
+__global__ void k_make_keys(int E, const int *src, const int *dst, unsigned long long *keys, int *indeg) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        keys[e] = (static_cast<unsigned long long>(static_cast<unsigned>(src[e])) << 32) |
+                  static_cast<unsigned>(dst[e]);
+        atomicAdd(&indeg[dst[e]], 1);
+    }
+}
+
+// Kahn from the sources (graph.py:274-288); *seen < V means a cycle.
+__global__ void __launch_bounds__(1024) k_kahn(int V, const int *obeg, const int *odst, int *deg, int *fa, int *fb,
+                                               int *seen) {
+    __shared__ int s_cur, s_next;
+    if (threadIdx.x == 0) s_cur = 0;
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += blockDim.x)
+        if (deg[v] == 0) fa[atomicAdd(&s_cur, 1)] = v;
+    __syncthreads();
+    int total = 0;
+    int *cur = fa, *nxt = fb;
+    for (;;) {
+        const int n = s_cur;
+        total += n;
+        if (n == 0) break;
+        if (threadIdx.x == 0) s_next = 0;
+        __syncthreads();
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            const int v = cur[t];
+            for (int q = obeg[v]; q < obeg[v + 1]; ++q)
+                if (atomicSub(&deg[odst[q]], 1) == 1) nxt[atomicAdd(&s_next, 1)] = odst[q];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_cur = s_next;
+        int *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *seen = total;
+}
+
+// Distinct current groups of the input successors of `t`, excluding `self`.
+// Returns the count, stopping early at 2 when `cap` == 2.
+__device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, const int *odst, int t, int self,
+                                          int *buf, int cap) {
+    int n = 0;
+    for (int q = obeg[t]; q < obeg[t + 1]; ++q) {
+        const int w = s.where[odst[q]];
+        if (w == self) continue;
+        bool dup = false;
+        for (int z = 0; z < n; ++z)
+            if (buf[z] == w) {
+                dup = true;
+                break;
+            }
+        if (dup) continue;
+        if (n == cap) return n + 1;
+        buf[n++] = w;
+    }
+    return n;
+}
+
+// The reference DFS (fusion.py:281-303), replayed exactly by one thread.
+__global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
+                      int *stack, int *buf) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int two[2];
+    for (int src = 0; src < V; ++src) {
+        if (indeg[src] != 0) continue;  // sources of the input graph, ascending id
+        int sp = 0;
+        stack[sp++] = src;
+        while (sp > 0) {
+            int cur = s.where[stack[--sp]];
+            if (s.visited[cur]) continue;
+            for (;;) {
+                // |out[cur]| == 1 ?  (fusion.py:291-294)
+                if (out_groups(s, obeg, odst, s.tail[cur], cur, two, 1) != 1) break;
+                const int nxt = two[0];
+                // _match_seqs(seqs[cur], seqs[nxt]) (fusion.py:93-104) via the trie
+                const int ln = s.len[nxt];
+                int st = s.state[cur];
+                if (st < 0 || ln > Lmax || s.len[cur] + ln > Lmax) break;
+                for (int q = 0; q < ln && st >= 0; ++q) st = trie_step(t, st, s.seq[static_cast<size_t>(nxt) * Lmax + q]);
+                if (st < 0) break;
+                const int fl = t.flags[st];
+                int kind;  // 2 prefix (wins), 1 full
+                if (fl & 2) kind = 2;
+                else if (fl & 1) kind = 1;
+                else break;
+                // combine(cur, nxt) (fusion.py:169-190)
+                const int nw = cur < nxt ? cur : nxt;
+                const int lc = s.len[cur];
+                int tmp[32];
+                const int L2 = lc + ln;
+                for (int q = 0; q < lc; ++q) tmp[q] = s.seq[static_cast<size_t>(cur) * Lmax + q];
+                for (int q = 0; q < ln; ++q) tmp[lc + q] = s.seq[static_cast<size_t>(nxt) * Lmax + q];
+                const int h_cur = s.head[cur], t_cur = s.tail[cur], h_nxt = s.head[nxt], t_nxt = s.tail[nxt];
+                // rename the members of the group whose id disappears
+                if (nw == cur) {
+                    for (int x = h_nxt;; x = s.next[x]) {
+                        s.where[x] = nw;
+                        if (x == t_nxt) break;
+                    }
+                } else {
+                    for (int x = h_cur;; x = s.next[x]) {
+                        s.where[x] = nw;
+                        if (x == t_cur) break;
+                    }
+                }
+                s.next[t_cur] = h_nxt;
+                s.head[nw] = h_cur;
+                s.tail[nw] = t_nxt;
+                s.len[nw] = L2;
+                for (int q = 0; q < L2; ++q) s.seq[static_cast<size_t>(nw) * Lmax + q] = tmp[q];
+                s.state[nw] = st;
+                s.tag[nw] = kind == 2 ? kTagBound : kTagFused;
+                cur = nw;
+            }
+            s.visited[cur] = 1;
+            // push unvisited out groups in descending id (fusion.py:301-303)
+            const int no = out_groups(s, obeg, odst, s.tail[cur], cur, buf, 0x7fffffff);
+            // insertion sort ascending (out-degrees are small; worst case is still exact)
+            for (int i = 1; i < no; ++i) {
+                const int v = buf[i];
+                int j = i - 1;
+                while (j >= 0 && buf[j] > v) {
+                    buf[j + 1] = buf[j];
+                    --j;
+                }
+                buf[j + 1] = v;
+            }
+            for (int z = no - 1; z >= 0; --z)
+                if (!s.visited[buf[z]]) stack[sp++] = buf[z];
+        }
+    }
+}
+
+// final_partition (fusion.py:195-219): one thread per surviving group.
+// og_rep[v] = representative (min index) of v's output group, og_pos[v] = its
+// position in chain order; og_tag/og_size are written at the representative.
+__global__ void k_final_partition(int V, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
+                                  DfsState s, int *og_rep, int *og_pos, int *og_tag, int *og_size) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < V; g += gridDim.x * blockDim.x) {
+        if (s.where[g] != g) continue;  // not a group id
+        const int tg = s.tag[g];
+        if (tg != kTagBound) {
+            int rep = V, k = 0;
+            for (int x = s.head[g];; x = s.next[x]) {
+                rep = x < rep ? x : rep;
+                if (x == s.tail[g]) break;
+            }
+            for (int x = s.head[g];; x = s.next[x]) {
+                og_rep[x] = rep;
+                og_pos[x] = k++;
+                if (x == s.tail[g]) break;
+            }
+            og_tag[rep] = tg;
+            og_size[rep] = k;
+            continue;
+        }
+        // longest member prefix whose concatenated type sequence is a rule
+        int best_k = 0, k = 0, st = 0;
+        for (int x = s.head[g];; x = s.next[x]) {
+            ++k;
+            for (int q = seq_beg[x]; q < seq_beg[x + 1]; ++q) st = trie_step(t, st, seq_types[q]);
+            if (st >= 0 && (t.flags[st] & 1)) best_k = k;
+            if (x == s.tail[g]) break;
+        }
+        int rep = V;
+        k = 0;
+        for (int x = s.head[g];; x = s.next[x]) {
+            if (k < best_k) rep = x < rep ? x : rep;
+            ++k;
+            if (x == s.tail[g]) break;
+        }
+        k = 0;
+        for (int x = s.head[g];; x = s.next[x]) {
+            if (k < best_k) {
+                og_rep[x] = rep;
+                og_pos[x] = k;
+            } else {
+                og_rep[x] = x;
+                og_pos[x] = 0;
+                og_tag[x] = tag_in[x];
+                og_size[x] = 1;
+            }
+            ++k;
+            if (x == s.tail[g]) break;
+        }
+        if (best_k >= 2) {
+            og_tag[rep] = kTagFused;
+            og_size[rep] = best_k;
+        } else if (best_k == 1) {
+            og_tag[rep] = tag_in[rep];
+            og_size[rep] = 1;
+        }
+    }
+}
+
+__global__ void k_rep_flags(int V, const int *og_rep, const int *og_size, int *is_rep, int *size_at) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const bool r = og_rep[v] == v;
+        is_rep[v] = r ? 1 : 0;
+        size_at[v] = r ? og_size[v] : 0;
+    }
+}
+
+// scatter members; grp_index[v] = exclusive scan of is_rep (valid at reps)
+__global__ void k_scatter(int V, const int *og_rep, const int *og_pos, const int *grp_index, const int *mem_off,
+                          int *members, int *grp_of_node) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const int r = og_rep[v];
+        const int z = grp_index[r];
+        members[mem_off[r] + og_pos[v]] = v;
+        grp_of_node[v] = z;
+    }
+}
+
+// Per output group: node index, tag, mem sum, costs (fusion.py:117-130,236-241).
+__global__ void k_group_values(int V, int D, const int *is_rep, const int *grp_index, const int *mem_off,
+                               const int *og_tag, const int *og_size, const int *members, const long long *mem_in,
+                               const double *cost_in, const int *seq_beg, const int *seq_types, int n_ov,
+                               const int *ov_beg, const int *ov_types, const int *ov_dev, const double *ov_time,
+                               int sum_mode, int *grp_node, int *grp_tag, int *grp_beg, long long *grp_mem,
+                               double *grp_cost) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        if (!is_rep[v]) continue;
+        const int z = grp_index[v];
+        const int b = mem_off[v], n = og_size[v];
+        grp_node[z] = v;
+        grp_tag[z] = og_tag[v];
+        grp_beg[z] = b;
+        long long m = 0;
+        for (int u = 0; u < n; ++u) m += mem_in[members[b + u]];
+        grp_mem[z] = m;
+        for (int k = 0; k < D; ++k) {
+            double val;
+            if (n == 1) {
+                val = cost_in[static_cast<size_t>(v) * D + k];
+            } else {
+                // override for the exact member type sequence (profiles.py:140-160)
+                bool hit = false;
+                double ov = 0.0;
+                for (int o = 0; o < n_ov && !hit; ++o) {
+                    if (ov_dev[o] != k) continue;
+                    int q = ov_beg[o];
+                    const int qe = ov_beg[o + 1];
+                    bool eq = true;
+                    for (int u = 0; u < n && eq; ++u) {
+                        const int x = members[b + u];
+                        for (int w = seq_beg[x]; w < seq_beg[x + 1]; ++w, ++q) {
+                            if (q >= qe || ov_types[q] != seq_types[w]) {
+                                eq = false;
+                                break;
+                            }
+                        }
+                    }
+                    if (eq && q == qe) {
+                        hit = true;
+                        ov = ov_time[o];
+                    }
+                }
+                if (hit) {
+                    val = ov;
+                } else {
+                    bool all = true;
+                    for (int u = 0; u < n; ++u)
+                        if (isnan(cost_in[static_cast<size_t>(members[b + u]) * D + k])) all = false;
+                    if (!all) {
+                        val = __longlong_as_double(0x7ff8000000000000LL);  // absent
+                    } else if (sum_mode == 1) {
+                        // CPython >= 3.12 sum(): 0 + x0, then Neumaier compensation
+                        double f = 0.0 + cost_in[static_cast<size_t>(members[b]) * D + k];
+                        double c = 0.0;
+                        for (int u = 1; u < n; ++u) {
+                            const double x = cost_in[static_cast<size_t>(members[b + u]) * D + k];
+                            const double tt = f + x;
+                            if (fabs(f) >= fabs(x)) c += (f - tt) + x;
+                            else c += (x - tt) + f;
+                            f = tt;
+                        }
+                        if (c != 0.0 && isfinite(c)) f += c;
+                        val = f;
+                    } else {
+                        double f = 0.0;
+                        for (int u = 0; u < n; ++u) f = f + cost_in[static_cast<size_t>(members[b + u]) * D + k];
+                        val = f;
+                    }
+                }
+            }
+            grp_cost[static_cast<size_t>(z) * D + k] = val;
+        }
+    }
+}
+
+__global__ void k_edge_keys(int E, const int *src, const int *dst, const int *grp_of, const long long *payload,
+                            unsigned long long *keys, long long *vals, int *n_keep) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const int gu = grp_of[src[e]], gv = grp_of[dst[e]];
+        if (gu == gv) {
+            keys[e] = ~0ULL;  // internal edge: sorts last, dropped
+            vals[e] = 0;
+        } else {
+            keys[e] = (static_cast<unsigned long long>(static_cast<unsigned>(gu)) << 32) | static_cast<unsigned>(gv);
+            vals[e] = payload[e];
+            atomicAdd(n_keep, 1);
+        }
+    }
+}
+
+__global__ void k_edge_split(int n, const unsigned long long *keys, int *u, int *v) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        u[e] = static_cast<int>(keys[e] >> 32);
+        v[e] = static_cast<int>(keys[e] & 0xffffffffULL);
+    }
+}
+
+struct Arena {
+    unsigned char *base = nullptr;
+    size_t used = 0, cap = 0;
+    template <typename T>
+    T *take(size_t n) {
+        const size_t at = (used + 255) & ~size_t(255);
+        used = at + std::max<size_t>(n, 1) * sizeof(T);
+        return reinterpret_cast<T *>(base + at);
+    }
+};
+
+}  // namespace
+
+extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coarsen_output *out, mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!in || !out) return cset_err(err, MP_ERR_INVALID, 0, 0, "null argument");
+    memset(out, 0, sizeof(*out));
+    const int V = in->n_nodes, E = in->n_edges, D = in->n_dev, R = in->n_rules, O = in->n_overrides;
+    if (V < 0 || E < 0 || D < 1 || R < 0 || O < 0) return cset_err(err, MP_ERR_INVALID, V, E, "bad sizes");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return cset_err(err, MP_ERR_NO_GPU, 0, 0, "no CUDA device");
+    CK(cudaSetDevice(device));
+    if (V == 0) return MP_OK;
+    const int S = in->seq_beg[V];
+    const int RT = R ? in->rule_beg[R] : 0;
+    const int OT = O ? in->ov_beg[O] : 0;
+    int Lmax = 1;
+    for (int r = 0; r < R; ++r) Lmax = std::max(Lmax, in->rule_beg[r + 1] - in->rule_beg[r]);
+    if (Lmax > 30) return cset_err(err, MP_ERR_UNSUPPORTED, Lmax, 30, "rule longer than 30 types");
+    for (int e = 0; e < E; ++e)
+        if (in->esrc[e] < 0 || in->esrc[e] >= V || in->edst[e] < 0 || in->edst[e] >= V)
+            return cset_err(err, MP_ERR_INVALID, e, 0, "edge %d has a bad endpoint", e);
+
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // ---- upload ------------------------------------------------------------------
+    const int TN = R * Lmax + 2;
+    // generous upper bound of every arena allocation below (each is 256-aligned)
+    size_t bytes = 96 * 512;
+    bytes += 4ULL * ((V + 1ULL) * 40 + 8ULL * E + S + RT + OT + 2ULL * O + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
+    bytes += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
+    size_t tmp_bytes = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (const unsigned long long *)nullptr,
+                                   (unsigned long long *)nullptr, std::max(E, 1));
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (const long long *)nullptr, (long long *)nullptr, std::max(E, 1));
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, (const int *)nullptr, (int *)nullptr, V + 1);
+    size_t t4 = 0;
+    cub::DeviceReduce::ReduceByKey(nullptr, t4, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                   (const long long *)nullptr, (long long *)nullptr, (int *)nullptr, cub::Sum(),
+                                   std::max(E, 1));
+    const size_t tmpb = std::max(std::max(tmp_bytes, t2), std::max(t3, t4)) + 256;
+    bytes += tmpb;
+    Arena ar;
+    CK(cudaMalloc(&ar.base, bytes));
+    ar.cap = bytes;
+    auto up = [&](auto *dst, const auto *src, size_t n) -> cudaError_t {
+        if (n == 0) return cudaSuccess;
+        return cudaMemcpyAsync(dst, src, n * sizeof(*src), cudaMemcpyHostToDevice, st);
+    };
+    int *d_seq_beg = ar.take<int>(V + 1), *d_seq = ar.take<int>(S), *d_tag = ar.take<int>(V);
+    long long *d_mem = ar.take<long long>(V);
+    double *d_cost = ar.take<double>(static_cast<size_t>(V) * D);
+    int *d_esrc = ar.take<int>(E), *d_edst = ar.take<int>(E);
+    long long *d_pay = ar.take<long long>(E);
+    int *d_rbeg = ar.take<int>(R + 1), *d_rt = ar.take<int>(RT);
+    int *d_obeg = ar.take<int>(O + 1), *d_ot = ar.take<int>(OT), *d_odev = ar.take<int>(O);
+    double *d_otime = ar.take<double>(O);
+    int rc = MP_OK;
+    CK(up(d_seq_beg, in->seq_beg, V + 1));
+    CK(up(d_seq, in->seq_types, S));
+    CK(up(d_tag, in->tag, V));
+    CK(up(d_mem, reinterpret_cast<const long long *>(in->mem), V));
+    CK(up(d_cost, in->cost, static_cast<size_t>(V) * D));
+    CK(up(d_esrc, in->esrc, E));
+    CK(up(d_edst, in->edst, E));
+    CK(up(d_pay, reinterpret_cast<const long long *>(in->payload), E));
+    if (R) {
+        CK(up(d_rbeg, in->rule_beg, R + 1));
+        CK(up(d_rt, in->rule_types, RT));
+    }
+    if (O) {
+        CK(up(d_obeg, in->ov_beg, O + 1));
+        CK(up(d_ot, in->ov_types, OT));
+        CK(up(d_odev, in->ov_dev, O));
+        CK(up(d_otime, in->ov_time, O));
+    }
+    const int grid = std::max(1, std::min(2048, (std::max(V, E) + 255) / 256));
+    // ---- K1a: CSR sorted by (src, dst), degrees, cycle check ------------------------
+    unsigned long long *keys = ar.take<unsigned long long>(E), *skeys = ar.take<unsigned long long>(E);
+    int *indeg = ar.take<int>(V + 1), *outcnt = ar.take<int>(V + 1), *obeg = ar.take<int>(V + 1);
+    int *odst = ar.take<int>(E);
+    int *deg = ar.take<int>(V + 1), *fa = ar.take<int>(V + 1), *fb = ar.take<int>(V + 1), *seen = ar.take<int>(4);
+    void *tmp = ar.take<unsigned char>(tmpb);
+    CK(cudaMemsetAsync(indeg, 0, 4ULL * (V + 1), st));
+    CK(cudaMemsetAsync(outcnt, 0, 4ULL * (V + 1), st));
+    if (E) {
+        k_make_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, keys, indeg);
+        ++g_mp_launches;
+        size_t tb = tmpb;
+        CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, skeys, E, 0, 64, st));
+        k_split_keys<<<grid, 256, 0, st>>>(E, skeys, odst, outcnt);
+        ++g_mp_launches;
+    }
+    {
+        size_t tb = tmpb;
+        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, outcnt, obeg, V + 1, st));
+    }
+    CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
+    k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, seen);
+    ++g_mp_launches;
+    int h_seen = 0;
+    CK(cudaMemcpyAsync(&h_seen, seen, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_seen != V) {
+        rc = cset_err(err, MP_ERR_CYCLE, V - h_seen, 0, "graph contains a cycle");
+    }
+    // ---- trie + node states -----------------------------------------------------------
+    Trie trie{};
+    trie.child = ar.take<int>(TN);
+    trie.sibling = ar.take<int>(TN);
+    trie.type = ar.take<int>(TN);
+    trie.flags = ar.take<int>(TN);
+    DfsState s{};
+    s.where = ar.take<int>(V);
+    s.next = ar.take<int>(V);
+    s.head = ar.take<int>(V);
+    s.tail = ar.take<int>(V);
+    s.state = ar.take<int>(V);
+    s.len = ar.take<int>(V);
+    s.seq = ar.take<int>(static_cast<size_t>(V) * Lmax);
+    s.tag = ar.take<int>(V);
+    s.visited = ar.take<unsigned char>(V);
+    int *stack = ar.take<int>(E + V + 8), *buf = ar.take<int>(E + V + 8);
+    int *ntrie = ar.take<int>(4);
+    if (rc == MP_OK) {
+        k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
+        ++g_mp_launches;
+        k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, s);
+        ++g_mp_launches;
+        // ---- K1b: the ordered DFS ------------------------------------------------------
+        k_dfs<<<1, 32, 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf);
+        ++g_mp_launches;
+        // ---- K2: final partition + materialize -----------------------------------------
+        int *og_rep = ar.take<int>(V), *og_pos = ar.take<int>(V), *og_tag = ar.take<int>(V), *og_size = ar.take<int>(V);
+        int *is_rep = ar.take<int>(V + 1), *size_at = ar.take<int>(V + 1), *grp_index = ar.take<int>(V + 1);
+        int *mem_off = ar.take<int>(V + 1), *members = ar.take<int>(V), *grp_of = ar.take<int>(V);
+        k_final_partition<<<grid, 256, 0, st>>>(V, d_seq_beg, d_seq, d_tag, trie, s, og_rep, og_pos, og_tag, og_size);
+        ++g_mp_launches;
+        k_rep_flags<<<grid, 256, 0, st>>>(V, og_rep, og_size, is_rep, size_at);
+        ++g_mp_launches;
+        CK(cudaMemsetAsync(is_rep + V, 0, 4, st));
+        CK(cudaMemsetAsync(size_at + V, 0, 4, st));
+        size_t tb = tmpb;
+        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, is_rep, grp_index, V + 1, st));
+        tb = tmpb;
+        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, size_at, mem_off, V + 1, st));
+        k_scatter<<<grid, 256, 0, st>>>(V, og_rep, og_pos, grp_index, mem_off, members, grp_of);
+        ++g_mp_launches;
+        int ng = 0;
+        CK(cudaMemcpyAsync(&ng, grp_index + V, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        int *grp_node = ar.take<int>(V), *grp_tag = ar.take<int>(V), *grp_beg = ar.take<int>(V + 1);
+        long long *grp_mem = ar.take<long long>(V);
+        double *grp_cost = ar.take<double>(static_cast<size_t>(V) * D);
+        k_group_values<<<grid, 256, 0, st>>>(V, D, is_rep, grp_index, mem_off, og_tag, og_size, members, d_mem, d_cost,
+                                             d_seq_beg, d_seq, O, d_obeg, d_ot, d_odev, d_otime, in->sum_mode, grp_node,
+                                             grp_tag, grp_beg, grp_mem, grp_cost);
+        ++g_mp_launches;
+        // quotient edges (fusion.py:242-247): keys (gu, gv) sorted, payloads summed
+        unsigned long long *ekeys = keys, *eskeys = skeys, *ukeys = ar.take<unsigned long long>(E);
+        long long *evals = ar.take<long long>(E), *esvals = ar.take<long long>(E), *usum = ar.take<long long>(E);
+        int *nkeep = ar.take<int>(4), *nuniq = ar.take<int>(4);
+        CK(cudaMemsetAsync(nkeep, 0, 4, st));
+        CK(cudaMemsetAsync(nuniq, 0, 4, st));
+        int h_keep = 0, h_uniq = 0;
+        if (E) {
+            k_edge_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, grp_of, d_pay, ekeys, evals, nkeep);
+            ++g_mp_launches;
+            tb = tmpb;
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ekeys, eskeys, evals, esvals, E, 0, 64, st));
+            CK(cudaMemcpyAsync(&h_keep, nkeep, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (h_keep > 0) {
+                tb = tmpb;
+                CK(cub::DeviceReduce::ReduceByKey(tmp, tb, eskeys, ukeys, esvals, usum, nuniq, cub::Sum(), h_keep, st));
+                CK(cudaMemcpyAsync(&h_uniq, nuniq, 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+            }
+        }
+        int *eu = ar.take<int>(std::max(h_uniq, 1));
+        int *ev = ar.take<int>(std::max(h_uniq, 1));
+        if (ar.used > ar.cap) {
+            rc = cset_err(err, MP_ERR_UNSUPPORTED, static_cast<int64_t>(ar.used), static_cast<int64_t>(ar.cap),
+                          "internal arena overflow");
+        } else {
+            if (h_uniq > 0) {
+                k_edge_split<<<grid, 256, 0, st>>>(h_uniq, ukeys, eu, ev);
+                ++g_mp_launches;
+            }
+            CK(cudaGetLastError());
+            // ---- download ---------------------------------------------------------------
+            out->n_groups = ng;
+            out->n_edges = h_uniq;
+            out->grp_node = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
+            out->grp_tag = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
+            out->mem_beg = static_cast<int32_t *>(malloc(4ULL * (ng + 1)));
+            out->members = static_cast<int32_t *>(malloc(4ULL * std::max(V, 1)));
+            out->grp_mem = static_cast<int64_t *>(malloc(8ULL * std::max(ng, 1)));
+            out->grp_cost = static_cast<double *>(malloc(8ULL * std::max(ng, 1) * D));
+            out->out_src = static_cast<int32_t *>(malloc(4ULL * std::max(h_uniq, 1)));
+            out->out_dst = static_cast<int32_t *>(malloc(4ULL * std::max(h_uniq, 1)));
+            out->out_payload = static_cast<int64_t *>(malloc(8ULL * std::max(h_uniq, 1)));
+            CK(cudaMemcpyAsync(out->grp_node, grp_node, 4ULL * ng, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->grp_tag, grp_tag, 4ULL * ng, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->mem_beg, grp_beg, 4ULL * ng, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->members, members, 4ULL * V, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->grp_mem, grp_mem, 8ULL * ng, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->grp_cost, grp_cost, 8ULL * ng * D, cudaMemcpyDeviceToHost, st));
+            if (h_uniq > 0) {
+                CK(cudaMemcpyAsync(out->out_src, eu, 4ULL * h_uniq, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(out->out_dst, ev, 4ULL * h_uniq, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(out->out_payload, usum, 8ULL * h_uniq, cudaMemcpyDeviceToHost, st));
+            }
+            CK(cudaStreamSynchronize(st));
+            out->mem_beg[ng] = V;
+        }
+    }
+    cudaFree(ar.base);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+extern "C" void mp_coarsen_free(mp_coarsen_output *out) {
+    if (!out) return;
+    free(out->grp_node);
+    free(out->grp_tag);
+    free(out->mem_beg);
+    free(out->members);
+    free(out->grp_mem);
+    free(out->grp_cost);
+    free(out->out_src);
+    free(out->out_dst);
+    free(out->out_payload);
+    memset(out, 0, sizeof(*out));
+}

@@ -1,0 +1,177 @@
+// mp_common.cuh — shared internals of libmoirai_b200 (sm_100a).
+//
+// Layout contract between the instance builder (mp_instance.cu) and the
+// evaluator kernels (mp_eval.cu).  Everything the evaluator reads for one
+// instance lives in ONE contiguous 16-byte-aligned "table blob" in HBM, so a
+// CTA stages it into shared memory with a single run of 1-D bulk-async (TMA)
+// copies completing on one mbarrier.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/moirai_b200.h"
+
+#define MP_CTA_MAX_THREADS 512
+#define MP_SMEM_OPTIN_MAX (227 * 1024)
+#define MP_SMEM_DYN_MAX (MP_SMEM_OPTIN_MAX - 8 * 1024)  // leaves room for static smem
+#define MP_NODE_BITS 20                 // node index field of a ready-entry meta word
+#define MP_NODE_MASK ((1u << MP_NODE_BITS) - 1u)
+#define MP_MAX_DEV 16                   // 3*K+1 clock slots must fit 6 bits
+#define MP_ROW_OVERFLOW 3               // internal: ready set exceeded on-chip capacity
+
+// Byte offsets of the sections of the instance table blob.
+struct TabOff {
+    uint32_t cost;      // f64 [n_ops*K]    p[i][k]                       (solver.py:61)
+    uint32_t mem;       // i64 [n_ops]      mem_bytes                     (solver.py:60)
+    uint32_t payload;   // f64 [n_flows]    (double)payload_bytes         (solver.py:65,77)
+    uint32_t bw;        // f64 [K*K]        effective bandwidth           (solver.py:66-67)
+    uint32_t cap;       // i64 [K]          device capacity               (solver.py:59)
+    uint32_t out_beg;   // u32 [n_ops+1]    CSR: out-flows of each op
+    uint32_t out_flow;  // u32 [n_flows]    flow indices grouped by source op
+    uint32_t fsrc;      // u32 [n_flows]    source op of each flow        (solver.py:63)
+    uint32_t fdst;      // u32 [n_flows]    destination op                 (solver.py:64)
+    uint32_t indeg;     // u16 [n_ops]      in-flows per op (npred seed, solver.py:109)
+    uint32_t lvl_ops;   // u32 [n_ops]      ops bucketed by height (0 = sinks)
+    uint32_t lvl_beg;   // u32 [n_ops+1]    level offsets into lvl_ops
+    uint32_t srcs;      // u32 [n_ops]      ops with no in-flow (initial ready set, solver.py:111)
+    uint32_t bytes;     // total, multiple of 16
+};
+
+// Byte offsets of one placement's dynamic state ("slot") — shared memory when
+// the instance is on-chip, a per-group global scratch slice otherwise.
+struct StOff {
+    uint32_t rank;      // f64 [n_ops]   downstream critical path of each op  (solver.py:100-107)
+    uint32_t est;       // f64 [n_ops]   earliest start from finished preds   (solver.py:110,142-143)
+    uint32_t clk;       // f64 [3K+1]    op_free | out_free | in_free | 0.0   (solver.py:112-114)
+    uint32_t load;      // u64 [K]       memory load per device               (solver.py:82-84)
+    uint32_t r_est;     // f64 [rcap]    ready entries: est part of the key
+    uint32_t r_rank;    // f64 [rcap]    ready entries: rank
+    uint32_t r_meta;    // u32 [rcap]    node | clock slot 1 << 20 | clock slot 2 << 26
+    uint32_t npred;     // u16 [n_ops]   unfinished in-flows                  (solver.py:109,141)
+    uint32_t dev;       // u8  [n_ops+32] placement row (16-byte-aligned copy, see dev_off)
+    uint32_t bytes;
+};
+
+struct EvalArgs {
+    const unsigned char *blob;   // instance tables (global)
+    TabOff to;
+    StOff so;
+    int n_ops, n_flows, K, n_levels, n_src, rcap;
+
+    // row source
+    const uint8_t *rows;          // LOAD: [n_rows][n_ops]
+    long long n_rows;             // rows in this launch
+    long long row_base;           // global index of rows[0]
+    long long out_base;           // output arrays are indexed by (global row - out_base)
+    const unsigned int *n_rows_dev;  // when set, the row count is read on the device
+    long long rows_bytes;         // readable bytes of `rows`
+    const uint32_t *enum_order;   // ENUM: op index per digit (most significant first)
+    const unsigned long long *enum_pow;  // ENUM: K^(n_ops-1-t)
+    unsigned long long enum_first;
+
+    // outputs (may be null)
+    double *makespan;
+    int8_t *status;
+    int32_t *mem_dev;
+    long long *overflow;
+    double *starts, *ends;        // TRACE
+    double *cta_best_ms;          // [gridDim.x] running per-CTA best (argmin)
+    long long *cta_best_row;
+    long long *ovf_rows;          // rows that overflowed the on-chip ready capacity
+    unsigned int *ovf_count;
+
+    unsigned long long *next;     // work counter (rows handed out)
+    unsigned char *gstate;        // global-state slots (off-chip mode)
+    int groups_per_cta;
+    int want_argmin;
+    int row_list;                 // 1: `row_idx` lists the global rows to (re)evaluate
+    const long long *row_idx;     // [n_rows] global row indices (row_list mode)
+};
+
+enum { SRC_LOAD = 0, SRC_ENUM = 1 };
+
+struct LsArgs {
+    const uint8_t *seed_rows;     // [n_seed][n_ops] device indices
+    int n_seed;
+    long long n_chains;
+    long long chain_base;         // global id of chain 0 (sharding across GPUs)
+    int moves;
+    unsigned long long rng_seed;
+    uint8_t *chain_rows;          // [n_chains][n_ops] final rows
+    double *chain_ms;             // [n_chains] final makespans (+inf infeasible)
+};
+
+// ---- small device helpers -------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA engine, SASS UBLKCP), completion
+// signalled as transaction bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MP_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MP_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+    return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+// Dispatch key order of the reference list scheduler (solver.py:126-129):
+// lexicographic min of (e, -rank, node).  All times are non-negative and never
+// -0.0, so IEEE order equals unsigned order of the bits.
+__device__ __forceinline__ bool key_less(unsigned long long e, unsigned long long r, uint32_t n,
+                                         unsigned long long be, unsigned long long br, uint32_t bn) {
+    return e < be || (e == be && (r > br || (r == br && n < bn)));
+}
+
+// ---- host-side launch plumbing (mp_eval.cu) ---------------------------------
+struct LaunchShape {
+    int G;                // lanes per placement
+    int groups_per_cta;
+    int threads;
+    int ctas;
+    int smem;             // dynamic smem bytes
+    bool onchip;
+};
+
+// Launches one evaluator variant; returns cudaError_t of the launch.
+cudaError_t mp_launch_eval(const LaunchShape &ls, int src_mode, bool trace, const EvalArgs &a,
+                           cudaStream_t s);
+cudaError_t mp_launch_finalize(const double *cta_ms, const long long *cta_row, int n, double *out_ms,
+                               long long *out_row, cudaStream_t s);
+cudaError_t mp_launch_ls(const LaunchShape &shape, const EvalArgs &a, const LsArgs &ls, cudaStream_t s);
+cudaError_t mp_launch_ls_pick(const double *chain_ms, long long n, double *out_ms, long long *out_c,
+                              cudaStream_t s);
+cudaError_t mp_eval_set_smem_limits();
+extern unsigned long long g_mp_launches;

@@ -1,0 +1,989 @@
+// mp_instance.cu — instance construction on the GPU and the C ABI entry points
+// for evaluation (mp_instance_create / mp_evaluate_* / mp_schedule_one /
+// mp_enumerate_argmin).
+//
+// mp_instance_create replaces `_Instance.__init__` (pkg/src/opplace/solver.py:45-72):
+// it uploads the flat tables once and derives everything the kernels need on the
+// device: fp64 payloads, in/out degrees, the out-flow CSR (stable radix sort by
+// source op), op-graph heights by a level-synchronous Kahn sweep from the sinks
+// (which doubles as the cycle check of `augment`/`topo_order`, graph.py:339-342),
+// height buckets for the rank pass, and the source list that seeds the ready set.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "mp_common.cuh"
+
+namespace {
+
+constexpr int kBuildThreads = 1024;
+
+inline uint32_t align16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~15ULL); }
+
+int set_err(mp_error *err, int code, int64_t a, int64_t b, const char *fmt, ...) {
+    if (err) {
+        err->code = code;
+        err->a = a;
+        err->b = b;
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define MP_CUDA(call)                                                                            \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return set_err(err, MP_ERR_CUDA, static_cast<int64_t>(e_), 0, "%s: %s (%s:%d)", #call, \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+    } while (0)
+
+// ---- build kernels ------------------------------------------------------------
+struct BuildErr {
+    unsigned long long missing;   // first (op*K + dev) with NaN cost
+    unsigned long long bad_flow;  // first flow with an endpoint out of range
+    unsigned int max_indeg;
+    unsigned int processed;       // ops given a height (== n_ops unless cyclic)
+    unsigned int n_levels;
+    unsigned int n_sinks;
+};
+
+__global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cost, const long long *mem,
+                                const int *fsrc, const int *fdst, const long long *payload,
+                                const long long *cap, const double *bw, unsigned char *blob, TabOff to,
+                                unsigned int *outdeg, unsigned int *indeg32, BuildErr *be) {
+    const int stride = gridDim.x * blockDim.x;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    double *bcost = reinterpret_cast<double *>(blob + to.cost);
+    long long *bmem = reinterpret_cast<long long *>(blob + to.mem);
+    double *bpay = reinterpret_cast<double *>(blob + to.payload);
+    double *bbw = reinterpret_cast<double *>(blob + to.bw);
+    long long *bcap = reinterpret_cast<long long *>(blob + to.cap);
+    uint32_t *bsrc = reinterpret_cast<uint32_t *>(blob + to.fsrc);
+    uint32_t *bdst = reinterpret_cast<uint32_t *>(blob + to.fdst);
+    const long long nc = static_cast<long long>(n_ops) * K;
+    for (long long x = t0; x < nc; x += stride) {
+        const double c = cost[x];
+        if (isnan(c)) atomicMin(&be->missing, static_cast<unsigned long long>(x));
+        bcost[x] = c;
+    }
+    for (int i = t0; i < n_ops; i += stride) bmem[i] = mem[i];
+    for (int k = t0; k < K * K; k += stride) bbw[k] = bw[k];
+    for (int k = t0; k < K; k += stride) bcap[k] = cap[k];
+    for (int f = t0; f < n_flows; f += stride) {
+        const int s = fsrc[f], d = fdst[f];
+        // Python int -> float conversion is correctly rounded, as is this cast.
+        bpay[f] = static_cast<double>(payload[f]);
+        if (s < 0 || s >= n_ops || d < 0 || d >= n_ops || s == d) {
+            atomicMin(&be->bad_flow, static_cast<unsigned long long>(f));
+            bsrc[f] = 0;
+            bdst[f] = 0;
+            continue;
+        }
+        bsrc[f] = static_cast<uint32_t>(s);
+        bdst[f] = static_cast<uint32_t>(d);
+        atomicAdd(&outdeg[s], 1u);
+        atomicAdd(&indeg32[d], 1u);
+    }
+}
+
+__global__ void k_indeg16(int n_ops, const unsigned int *indeg32, unsigned char *blob, TabOff to,
+                          unsigned char *is_src, BuildErr *be) {
+    uint16_t *b = reinterpret_cast<uint16_t *>(blob + to.indeg);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += gridDim.x * blockDim.x) {
+        const unsigned int d = indeg32[i];
+        atomicMax(&be->max_indeg, d);
+        b[i] = static_cast<uint16_t>(d > 65535u ? 65535u : d);
+        is_src[i] = d == 0 ? 1 : 0;
+    }
+}
+
+__global__ void k_iota(int n, unsigned int *v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v[i] = static_cast<unsigned int>(i);
+}
+
+// Level-synchronous Kahn sweep from the sinks of the op graph: height(i) =
+// 0 for ops with no out-flow, else 1 + max height of its consumers.  One CTA;
+// frontier lists ping-pong in global memory.  Ops never reached lie on or
+// above a cycle.
+__global__ void __launch_bounds__(kBuildThreads) k_heights(int n_ops, const unsigned int *in_beg,
+                                                           const unsigned int *in_flow,
+                                                           const uint32_t *fsrc, unsigned int *outcnt,
+                                                           unsigned int *height, unsigned int *fa,
+                                                           unsigned int *fb, BuildErr *be) {
+    __shared__ unsigned int s_next, s_cur;
+    if (threadIdx.x == 0) s_cur = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_ops; i += blockDim.x) {
+        if (outcnt[i] == 0) {
+            height[i] = 0;
+            fa[atomicAdd(&s_cur, 1u)] = static_cast<unsigned int>(i);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) be->n_sinks = s_cur;
+    unsigned int total = 0;
+    unsigned int h = 0;
+    unsigned int *cur = fa, *nxt = fb;
+    while (true) {
+        const unsigned int n = s_cur;
+        total += n;
+        if (n == 0) break;
+        if (threadIdx.x == 0) s_next = 0;
+        __syncthreads();
+        for (unsigned int t = threadIdx.x; t < n; t += blockDim.x) {
+            const unsigned int i = cur[t];
+            for (unsigned int q = in_beg[i]; q < in_beg[i + 1]; ++q) {
+                const unsigned int u = fsrc[in_flow[q]];
+                if (atomicSub(&outcnt[u], 1u) == 1u) {
+                    height[u] = h + 1;
+                    nxt[atomicAdd(&s_next, 1u)] = u;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_cur = s_next;
+        unsigned int *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ++h;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        be->processed = total;
+        be->n_levels = h;
+    }
+}
+
+__global__ void k_level_bounds(int n_ops, const unsigned int *sorted_h, unsigned int *lvl_beg, unsigned int n_levels) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_ops; t += gridDim.x * blockDim.x) {
+        const unsigned int h = sorted_h[t];
+        if (t == 0) {
+            for (unsigned int x = 0; x <= h; ++x) lvl_beg[x] = 0;
+        } else {
+            const unsigned int hp = sorted_h[t - 1];
+            for (unsigned int x = hp + 1; x <= h; ++x) lvl_beg[x] = static_cast<unsigned int>(t);
+        }
+        if (t == n_ops - 1) {
+            for (unsigned int x = h + 1; x <= n_levels; ++x) lvl_beg[x] = static_cast<unsigned int>(n_ops);
+        }
+    }
+}
+
+// Evaluator variants that are on-chip need their slot offsets; both kinds use this.
+StOff make_stoff(int n_ops, int K, int rcap) {
+    StOff s{};
+    uint64_t o = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint32_t at = static_cast<uint32_t>(o);
+        o = align16(o + bytes);
+        return at;
+    };
+    s.rank = take(8ULL * n_ops);
+    s.est = take(8ULL * n_ops);
+    s.clk = take(8ULL * (3 * K + 1));
+    s.load = take(8ULL * K);
+    s.r_est = take(8ULL * rcap);
+    s.r_rank = take(8ULL * rcap);
+    s.r_meta = take(4ULL * rcap);
+    s.npred = take(2ULL * n_ops);
+    s.dev = take(static_cast<uint64_t>(n_ops) + 32);
+    s.bytes = static_cast<uint32_t>(o);
+    return s;
+}
+
+TabOff make_taboff(int n_ops, int n_flows, int K) {
+    TabOff t{};
+    uint64_t o = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint32_t at = static_cast<uint32_t>(o);
+        o = align16(o + bytes);
+        return at;
+    };
+    t.cost = take(8ULL * n_ops * K);
+    t.mem = take(8ULL * n_ops);
+    t.payload = take(8ULL * n_flows);
+    t.bw = take(8ULL * K * K);
+    t.cap = take(8ULL * K);
+    t.out_beg = take(4ULL * (n_ops + 1));
+    t.out_flow = take(4ULL * n_flows);
+    t.fsrc = take(4ULL * n_flows);
+    t.fdst = take(4ULL * n_flows);
+    t.indeg = take(2ULL * n_ops);
+    t.lvl_ops = take(4ULL * n_ops);
+    t.lvl_beg = take(4ULL * (n_ops + 1));
+    t.srcs = take(4ULL * n_ops);
+    t.bytes = static_cast<uint32_t>(o);
+    return t;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) n = bytes;
+        return e;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+struct mp_instance {
+    int device = 0;
+    int n_ops = 0, n_flows = 0, K = 0, n_nodes = 0;
+    int n_levels = 0, n_src = 0, n_sinks = 0;
+    int ready_bound = 0;   // min-path-cover bound on any ready set
+    int sms = 0;
+    TabOff to{};
+    unsigned char *blob = nullptr;
+    // main (on-chip when possible) and off-chip variants
+    LaunchShape main{};
+    StOff main_so{};
+    int main_rcap = 0;
+    LaunchShape wide{};
+    StOff wide_so{};
+    DevBuf main_state, wide_state;
+    // per-call scratch
+    DevBuf ctrs;      // [0] main next, [1] wide next, [2] ovf count (u32) ...
+    DevBuf cta_best;  // ms[] then rows[]
+    DevBuf ovf_rows;
+    DevBuf rows_dev[2];
+    DevBuf out_dev[2];
+    DevBuf small;     // argmin result / enum tables / trace
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    cudaEvent_t ev_copy[2]{}, ev_used[2]{};
+    std::mutex mu;
+};
+
+namespace {
+
+void choose_shapes(mp_instance *I, int G_req, int ctas_per_sm_req) {
+    const int n_ops = I->n_ops, K = I->K;
+    const int smem_cap = MP_SMEM_DYN_MAX;
+    // Ready sets are antichains of the augmented DAG, so a vertex-disjoint path
+    // cover bounds them: every non-sink op continues into one out-flow and every
+    // non-source op is continued by one in-flow -> n_flows - n_ops + n_src + n_sinks
+    // paths.  Within 256 the bound is the on-chip capacity (no overflow possible);
+    // above it, 128 slots plus the off-chip re-run of overflowing rows.
+    int rcap = I->ready_bound <= 256 ? std::max(1, I->ready_bound) : 128;
+    StOff so = make_stoff(n_ops, K, rcap);
+    int G = G_req > 0 ? G_req : 8;
+    const int per_warp = 32 / G;
+    const long long avail = static_cast<long long>(smem_cap) - I->to.bytes;
+    long long groups_fit = avail > 0 ? avail / so.bytes : 0;
+    int warps = static_cast<int>(std::min<long long>(groups_fit / per_warp, MP_CTA_MAX_THREADS / 32));
+    if (warps >= 1) {
+        LaunchShape ls{};
+        ls.G = G;
+        ls.threads = warps * 32;
+        ls.groups_per_cta = ls.threads / G;
+        ls.smem = static_cast<int>(I->to.bytes + static_cast<long long>(ls.groups_per_cta) * so.bytes);
+        ls.onchip = true;
+        // static smem of the kernel is ~2 KB; 228 KB per SM in total
+        int per_sm = std::max(1, (228 * 1024) / (ls.smem + 3 * 1024));
+        per_sm = std::min(per_sm, 2048 / ls.threads);
+        if (ctas_per_sm_req > 0) per_sm = std::min(per_sm, ctas_per_sm_req);
+        ls.ctas = I->sms * per_sm;
+        I->main = ls;
+        I->main_so = so;
+        I->main_rcap = rcap;
+    } else {
+        I->main.onchip = false;
+    }
+    // off-chip variant: one warp per placement, full ready capacity
+    StOff wso = make_stoff(n_ops, K, std::max(1, I->ready_bound));
+    LaunchShape w{};
+    w.G = 32;
+    w.threads = 256;
+    w.groups_per_cta = 8;
+    w.onchip = false;
+    w.smem = 0;
+    // bound the scratch to ~8 GiB
+    long long groups = static_cast<long long>(I->sms) * 8;
+    const long long budget = 8LL << 30;
+    while (groups > 8 && groups * static_cast<long long>(wso.bytes) > budget) groups /= 2;
+    w.ctas = static_cast<int>(std::max(1LL, groups / 8));
+    I->wide = w;
+    I->wide_so = wso;
+    if (!I->main.onchip) {
+        I->main = w;
+        I->main_so = wso;
+        I->main_rcap = std::max(1, I->ready_bound);
+    }
+}
+
+EvalArgs base_args(const mp_instance *I, bool wide) {
+    EvalArgs a{};
+    a.blob = I->blob;
+    a.to = I->to;
+    a.so = wide ? I->wide_so : I->main_so;
+    a.n_ops = I->n_ops;
+    a.n_flows = I->n_flows;
+    a.K = I->K;
+    a.n_levels = I->n_levels;
+    a.n_src = I->n_src;
+    a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
+    a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
+    a.gstate = static_cast<unsigned char *>(wide ? I->wide_state.p : I->main_state.p);
+    return a;
+}
+
+}  // namespace
+
+// ================================================================================
+extern "C" {
+
+int32_t mp_abi_version(void) { return MP_ABI_VERSION; }
+
+int32_t mp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int64_t mp_launch_count(void) { return static_cast<int64_t>(g_mp_launches); }
+
+int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance **out, mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!prob || !out) return set_err(err, MP_ERR_INVALID, 0, 0, "null argument");
+    *out = nullptr;
+    const int n_ops = prob->n_ops, n_flows = prob->n_flows, K = prob->n_dev;
+    if (n_ops <= 0) return set_err(err, MP_ERR_EMPTY_GRAPH, 0, 0, "cannot place an empty graph");
+    if (K <= 0) return set_err(err, MP_ERR_INVALID, K, 0, "cluster has no devices");
+    if (K > MP_MAX_DEV) return set_err(err, MP_ERR_UNSUPPORTED, K, MP_MAX_DEV, "%d devices > %d", K, MP_MAX_DEV);
+    if (n_flows < 0) return set_err(err, MP_ERR_INVALID, n_flows, 0, "negative flow count");
+    if (static_cast<long long>(n_ops) + n_flows > static_cast<long long>(MP_NODE_MASK))
+        return set_err(err, MP_ERR_UNSUPPORTED, n_ops + static_cast<long long>(n_flows), MP_NODE_MASK,
+                       "augmented graph too large");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_err(err, MP_ERR_NO_GPU, 0, 0, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return set_err(err, MP_ERR_INVALID, device, ndev, "bad device ordinal");
+    MP_CUDA(cudaSetDevice(device));
+    MP_CUDA(mp_eval_set_smem_limits());
+    // total memory must fit int64 (the reference uses unbounded ints, solver.py:82-84)
+    {
+        long double tot = 0;
+        for (int i = 0; i < n_ops; ++i) {
+            if (prob->mem[i] < 0) return set_err(err, MP_ERR_INVALID, i, prob->mem[i], "negative mem_bytes");
+            tot += static_cast<long double>(prob->mem[i]);
+        }
+        if (tot >= 9.2e18L) return set_err(err, MP_ERR_UNSUPPORTED, 0, 0, "total mem_bytes exceeds int64");
+    }
+
+    mp_instance *I = new mp_instance();
+    I->device = device;
+    I->n_ops = n_ops;
+    I->n_flows = n_flows;
+    I->K = K;
+    I->n_nodes = n_ops + n_flows;
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, device);
+    I->sms = prop.multiProcessorCount;
+    I->to = make_taboff(n_ops, n_flows, K);
+
+    auto fail = [&](int code) {
+        mp_instance_destroy(I);
+        return code;
+    };
+#define MP_CUDA_I(call)                                                                                \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess)                                                                         \
+            return fail(set_err(err, MP_ERR_CUDA, static_cast<int64_t>(e_), 0, "%s: %s (%s:%d)", #call, \
+                                cudaGetErrorString(e_), __FILE__, __LINE__));                          \
+    } while (0)
+
+    MP_CUDA_I(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+    MP_CUDA_I(cudaStreamCreateWithFlags(&I->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        MP_CUDA_I(cudaEventCreateWithFlags(&I->ev_copy[k], cudaEventDisableTiming));
+        MP_CUDA_I(cudaEventCreateWithFlags(&I->ev_used[k], cudaEventDisableTiming));
+    }
+    MP_CUDA_I(cudaMalloc(&I->blob, I->to.bytes));
+    MP_CUDA_I(cudaMemsetAsync(I->blob, 0, I->to.bytes, I->stream));
+
+    // ---- upload raw arrays -------------------------------------------------
+    const size_t b_cost = 8ULL * n_ops * K, b_mem = 8ULL * n_ops, b_f = 4ULL * n_flows, b_pay = 8ULL * n_flows,
+                 b_cap = 8ULL * K, b_bw = 8ULL * K * K;
+    size_t off_cost = 0, off_mem = align16(off_cost + b_cost), off_src = align16(off_mem + b_mem),
+           off_dst = align16(off_src + b_f), off_pay = align16(off_dst + b_f), off_cap = align16(off_pay + b_pay),
+           off_bw = align16(off_cap + b_cap), raw_bytes = align16(off_bw + b_bw);
+    std::vector<unsigned char> host(raw_bytes, 0);
+    memcpy(host.data() + off_cost, prob->cost, b_cost);
+    memcpy(host.data() + off_mem, prob->mem, b_mem);
+    if (n_flows) {
+        memcpy(host.data() + off_src, prob->flow_src, b_f);
+        memcpy(host.data() + off_dst, prob->flow_dst, b_f);
+        memcpy(host.data() + off_pay, prob->payload, b_pay);
+    }
+    memcpy(host.data() + off_cap, prob->cap, b_cap);
+    memcpy(host.data() + off_bw, prob->bw, b_bw);
+
+    // scratch: raw | outdeg | indeg32 | outcnt | height | fa | fb | iota | sorted keys/vals | is_src | cub tmp | err
+    const size_t nA = static_cast<size_t>(n_ops) + 1, nF = static_cast<size_t>(std::max(n_flows, 1));
+    size_t s_outdeg = raw_bytes, s_indeg = align16(s_outdeg + 4 * nA), s_outcnt = align16(s_indeg + 4 * nA),
+           s_height = align16(s_outcnt + 4 * nA), s_fa = align16(s_height + 4 * nA), s_fb = align16(s_fa + 4 * nA),
+           s_iota = align16(s_fb + 4 * nA), s_keys = align16(s_iota + 4 * std::max(nA, nF)),
+           s_in_beg = align16(s_keys + 4 * std::max(nA, nF)), s_in_flow = align16(s_in_beg + 4 * nA),
+           s_issrc = align16(s_in_flow + 4 * nF), s_nsel = align16(s_issrc + nA), s_err = align16(s_nsel + 16),
+           s_tmp = align16(s_err + sizeof(BuildErr));
+    // cub temp size
+    size_t tmp1 = 0, tmp2 = 0, tmp3 = 0, tmp4 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp1, (const unsigned int *)nullptr, (unsigned int *)nullptr,
+                                    (const unsigned int *)nullptr, (unsigned int *)nullptr, static_cast<int>(nF));
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp2, (const unsigned int *)nullptr, (unsigned int *)nullptr,
+                                    (const unsigned int *)nullptr, (unsigned int *)nullptr, static_cast<int>(nA));
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp3, (const unsigned int *)nullptr, (unsigned int *)nullptr,
+                                  static_cast<int>(nA));
+    cub::DeviceSelect::Flagged(nullptr, tmp4, (const unsigned int *)nullptr, (const unsigned char *)nullptr,
+                               (unsigned int *)nullptr, (int *)nullptr, n_ops);
+    const size_t tmpb = std::max(std::max(tmp1, tmp2), std::max(tmp3, tmp4)) + 256;
+    const size_t scratch_bytes = s_tmp + tmpb;
+    DevBuf scratch;
+    MP_CUDA_I(scratch.ensure(scratch_bytes));
+    unsigned char *S = static_cast<unsigned char *>(scratch.p);
+    MP_CUDA_I(cudaMemsetAsync(S + raw_bytes, 0, scratch_bytes - raw_bytes, I->stream));
+    MP_CUDA_I(cudaMemcpyAsync(S, host.data(), raw_bytes, cudaMemcpyHostToDevice, I->stream));
+    BuildErr *d_be = reinterpret_cast<BuildErr *>(S + s_err);
+    {
+        BuildErr init{};
+        init.missing = ~0ULL;
+        init.bad_flow = ~0ULL;
+        MP_CUDA_I(cudaMemcpyAsync(d_be, &init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
+    }
+    unsigned int *outdeg = reinterpret_cast<unsigned int *>(S + s_outdeg);
+    unsigned int *indeg32 = reinterpret_cast<unsigned int *>(S + s_indeg);
+    unsigned int *outcnt = reinterpret_cast<unsigned int *>(S + s_outcnt);
+    unsigned int *height = reinterpret_cast<unsigned int *>(S + s_height);
+    unsigned int *fa = reinterpret_cast<unsigned int *>(S + s_fa);
+    unsigned int *fb = reinterpret_cast<unsigned int *>(S + s_fb);
+    unsigned int *iota = reinterpret_cast<unsigned int *>(S + s_iota);
+    unsigned int *keys = reinterpret_cast<unsigned int *>(S + s_keys);
+    unsigned int *in_beg = reinterpret_cast<unsigned int *>(S + s_in_beg);
+    unsigned int *in_flow = reinterpret_cast<unsigned int *>(S + s_in_flow);
+    unsigned char *is_src = S + s_issrc;
+    int *nsel = reinterpret_cast<int *>(S + s_nsel);
+    void *tmp = S + s_tmp;
+
+    const int gridN = std::max(1, std::min(1024, (std::max(n_ops * K, n_flows) + 255) / 256));
+    k_copy_validate<<<gridN, 256, 0, I->stream>>>(
+        n_ops, n_flows, K, reinterpret_cast<const double *>(S + off_cost),
+        reinterpret_cast<const long long *>(S + off_mem), reinterpret_cast<const int *>(S + off_src),
+        reinterpret_cast<const int *>(S + off_dst), reinterpret_cast<const long long *>(S + off_pay),
+        reinterpret_cast<const long long *>(S + off_cap), reinterpret_cast<const double *>(S + off_bw), I->blob,
+        I->to, outdeg, indeg32, d_be);
+    ++g_mp_launches;
+    MP_CUDA_I(cudaGetLastError());
+    k_indeg16<<<gridN, 256, 0, I->stream>>>(n_ops, indeg32, I->blob, I->to, is_src, d_be);
+    ++g_mp_launches;
+    BuildErr be{};
+    MP_CUDA_I(cudaMemcpyAsync(&be, d_be, sizeof(be), cudaMemcpyDeviceToHost, I->stream));
+    MP_CUDA_I(cudaStreamSynchronize(I->stream));
+    if (be.missing != ~0ULL)
+        return fail(set_err(err, MP_ERR_MISSING_COST, static_cast<int64_t>(be.missing / K),
+                            static_cast<int64_t>(be.missing % K), "op index %lld has no compute time for device index %lld",
+                            static_cast<long long>(be.missing / K), static_cast<long long>(be.missing % K)));
+    if (be.bad_flow != ~0ULL)
+        return fail(set_err(err, MP_ERR_INVALID, static_cast<int64_t>(be.bad_flow), 0, "flow %lld has a bad endpoint",
+                            static_cast<long long>(be.bad_flow)));
+    if (be.max_indeg > 65535u)
+        return fail(set_err(err, MP_ERR_UNSUPPORTED, be.max_indeg, 65535, "op in-degree %u > 65535", be.max_indeg));
+
+    uint32_t *b_out_beg = reinterpret_cast<uint32_t *>(I->blob + I->to.out_beg);
+    uint32_t *b_out_flow = reinterpret_cast<uint32_t *>(I->blob + I->to.out_flow);
+    const uint32_t *b_fsrc = reinterpret_cast<const uint32_t *>(I->blob + I->to.fsrc);
+    const uint32_t *b_fdst = reinterpret_cast<const uint32_t *>(I->blob + I->to.fdst);
+    uint32_t *b_lvl_ops = reinterpret_cast<uint32_t *>(I->blob + I->to.lvl_ops);
+    uint32_t *b_lvl_beg = reinterpret_cast<uint32_t *>(I->blob + I->to.lvl_beg);
+    uint32_t *b_srcs = reinterpret_cast<uint32_t *>(I->blob + I->to.srcs);
+
+    // out-flow CSR: exclusive scan of out-degrees, stable sort of flows by source
+    size_t tb = tmpb;
+    MP_CUDA_I(cub::DeviceScan::ExclusiveSum(tmp, tb, outdeg, b_out_beg, n_ops + 1, I->stream));
+    tb = tmpb;
+    MP_CUDA_I(cub::DeviceScan::ExclusiveSum(tmp, tb, indeg32, in_beg, n_ops + 1, I->stream));
+    if (n_flows > 0) {
+        k_iota<<<gridN, 256, 0, I->stream>>>(n_flows, iota);
+        ++g_mp_launches;
+        tb = tmpb;
+        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, b_fsrc, keys, iota, b_out_flow, n_flows, 0, 32, I->stream));
+        tb = tmpb;
+        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, b_fdst, keys, iota, in_flow, n_flows, 0, 32, I->stream));
+    }
+    // heights (rank-pass levels) + cycle check
+    MP_CUDA_I(cudaMemcpyAsync(outcnt, outdeg, 4ULL * n_ops, cudaMemcpyDeviceToDevice, I->stream));
+    k_heights<<<1, kBuildThreads, 0, I->stream>>>(n_ops, in_beg, in_flow, b_fsrc, outcnt, height, fa, fb, d_be);
+    ++g_mp_launches;
+    MP_CUDA_I(cudaMemcpyAsync(&be, d_be, sizeof(be), cudaMemcpyDeviceToHost, I->stream));
+    MP_CUDA_I(cudaStreamSynchronize(I->stream));
+    if (be.processed != static_cast<unsigned int>(n_ops))
+        return fail(set_err(err, MP_ERR_CYCLE, n_ops - static_cast<int64_t>(be.processed), 0,
+                            "graph contains a cycle"));
+    I->n_levels = static_cast<int>(be.n_levels);
+    // bucket ops by height (stable: ascending op index inside a level)
+    k_iota<<<gridN, 256, 0, I->stream>>>(n_ops, iota);
+    ++g_mp_launches;
+    tb = tmpb;
+    MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, height, keys, iota, b_lvl_ops, n_ops, 0, 32, I->stream));
+    k_level_bounds<<<gridN, 256, 0, I->stream>>>(n_ops, keys, b_lvl_beg, be.n_levels);
+    ++g_mp_launches;
+    // initial ready set: ops without in-flows, ascending
+    tb = tmpb;
+    MP_CUDA_I(cub::DeviceSelect::Flagged(tmp, tb, iota, is_src, b_srcs, nsel, n_ops, I->stream));
+    int h_nsel = 0;
+    MP_CUDA_I(cudaMemcpyAsync(&h_nsel, nsel, sizeof(int), cudaMemcpyDeviceToHost, I->stream));
+    MP_CUDA_I(cudaStreamSynchronize(I->stream));
+    I->n_src = h_nsel;
+    I->n_sinks = static_cast<int>(be.n_sinks);
+    I->ready_bound = std::min(I->n_nodes, n_flows - n_ops + I->n_src + I->n_sinks);
+
+    choose_shapes(I, 0, 0);
+    *out = I;
+    return MP_OK;
+#undef MP_CUDA_I
+}
+
+void mp_instance_destroy(mp_instance *I) {
+    if (!I) return;
+    cudaSetDevice(I->device);
+    if (I->stream) cudaStreamSynchronize(I->stream);
+    if (I->copy_stream) cudaStreamSynchronize(I->copy_stream);
+    if (I->blob) cudaFree(I->blob);
+    for (int k = 0; k < 2; ++k) {
+        if (I->ev_copy[k]) cudaEventDestroy(I->ev_copy[k]);
+        if (I->ev_used[k]) cudaEventDestroy(I->ev_used[k]);
+    }
+    if (I->stream) cudaStreamDestroy(I->stream);
+    if (I->copy_stream) cudaStreamDestroy(I->copy_stream);
+    delete I;
+}
+
+int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
+    if (!I || !info) return MP_ERR_INVALID;
+    info->n_ops = I->n_ops;
+    info->n_flows = I->n_flows;
+    info->n_dev = I->K;
+    info->n_levels = I->n_levels;
+    info->n_sources = I->n_src;
+    info->ready_cap = I->main_rcap;
+    info->group_lanes = I->main.G;
+    info->groups_per_cta = I->main.groups_per_cta;
+    info->ctas = I->main.ctas;
+    info->smem_bytes = I->main.onchip ? I->main.smem : 0;
+    info->onchip = I->main.onchip ? 1 : 0;
+    info->device = I->device;
+    info->table_bytes = I->to.bytes;
+    info->state_bytes = I->main_so.bytes;
+    return MP_OK;
+}
+
+int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t ctas_per_sm) {
+    if (!I) return MP_ERR_INVALID;
+    if (group_lanes != 0 && group_lanes != 4 && group_lanes != 8 && group_lanes != 16 && group_lanes != 32)
+        return MP_ERR_INVALID;
+    std::lock_guard<std::mutex> lk(I->mu);
+    choose_shapes(I, group_lanes, ctas_per_sm);
+    return MP_OK;
+}
+
+}  // extern "C"
+
+// ---- evaluation plumbing ------------------------------------------------------
+namespace {
+
+// counters layout (u64 words): [0] main next, [1] wide next, [2] ovf count (u32 in low half)
+cudaError_t prepare(mp_instance *I, bool argmin, long long max_rows) {
+    cudaError_t e;
+    if (!I->main.onchip) {
+        e = I->main_state.ensure(static_cast<size_t>(I->main.ctas) * I->main.groups_per_cta * I->main_so.bytes);
+        if (e != cudaSuccess) return e;
+    }
+    if ((e = I->ctrs.ensure(64)) != cudaSuccess) return e;
+    const int nb = I->main.ctas + I->wide.ctas;
+    if ((e = I->cta_best.ensure(static_cast<size_t>(nb) * 16 + 64)) != cudaSuccess) return e;
+    if (I->main_rcap < I->ready_bound) {
+        e = I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes);
+        if (e != cudaSuccess) return e;
+        e = I->ovf_rows.ensure(static_cast<size_t>(std::max(1LL, max_rows)) * 8);
+        if (e != cudaSuccess) return e;
+    }
+    (void)argmin;
+    return cudaSuccess;
+}
+
+__global__ void k_init_best(double *ms, long long *row, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        ms[i] = __builtin_huge_val();
+        row[i] = LLONG_MAX;
+    }
+}
+
+double *best_ms_arr(mp_instance *I) { return static_cast<double *>(I->cta_best.p); }
+long long *best_row_arr(mp_instance *I) {
+    return reinterpret_cast<long long *>(static_cast<unsigned char *>(I->cta_best.p) +
+                                         static_cast<size_t>(I->main.ctas + I->wide.ctas) * 8);
+}
+
+// One evaluation pass over rows[0..n) (device pointers), outputs indexed from out_base.
+cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long row_base, long long out_base,
+                     long long rows_bytes, double *ms, int8_t *st, int32_t *md, long long *ov, bool argmin,
+                     cudaStream_t s) {
+    unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
+    cudaError_t e = cudaMemsetAsync(ctr, 0, 64, s);
+    if (e != cudaSuccess) return e;
+    EvalArgs a = base_args(I, false);
+    a.rows = rows;
+    a.n_rows = n;
+    a.row_base = row_base;
+    a.out_base = out_base;
+    a.rows_bytes = rows_bytes;
+    a.makespan = ms;
+    a.status = st;
+    a.mem_dev = md;
+    a.overflow = ov;
+    a.cta_best_ms = best_ms_arr(I);
+    a.cta_best_row = best_row_arr(I);
+    a.want_argmin = argmin ? 1 : 0;
+    a.next = ctr;
+    a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
+    a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) return e;
+    if (I->main_rcap < I->ready_bound) {
+        // rows whose ready set outgrew the on-chip capacity: re-run off-chip
+        EvalArgs b = base_args(I, true);
+        b.rows = rows;
+        b.n_rows = 0;
+        b.n_rows_dev = reinterpret_cast<const unsigned int *>(ctr + 2);
+        b.row_list = 1;
+        b.row_idx = static_cast<const long long *>(I->ovf_rows.p);
+        b.row_base = row_base;
+        b.out_base = out_base;
+        b.rows_bytes = rows_bytes;
+        b.makespan = ms;
+        b.status = st;
+        b.mem_dev = md;
+        b.overflow = ov;
+        b.cta_best_ms = best_ms_arr(I) + I->main.ctas;
+        b.cta_best_row = best_row_arr(I) + I->main.ctas;
+        b.want_argmin = argmin ? 1 : 0;
+        b.next = ctr + 1;
+        b.ovf_count = reinterpret_cast<unsigned int *>(ctr + 3);
+        b.ovf_rows = static_cast<long long *>(I->ovf_rows.p);  // never written (rcap = all nodes)
+        if ((e = mp_launch_eval(I->wide, SRC_LOAD, false, b, s)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int evaluate_impl(mp_instance *I, const uint8_t *rows, long long n_rows, double *makespan, int8_t *status,
+                  int32_t *mem_dev, int64_t *overflow, bool argmin, int64_t *best_row, double *best_ms,
+                  uint32_t flags, void *stream, mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!I) return set_err(err, MP_ERR_INVALID, 0, 0, "null instance");
+    if (n_rows < 0) return set_err(err, MP_ERR_INVALID, n_rows, 0, "negative row count");
+    std::lock_guard<std::mutex> lk(I->mu);
+    MP_CUDA(cudaSetDevice(I->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : I->stream;
+    const long long row_bytes = I->n_ops;
+    const bool devptr = (flags & MP_DEVICE_PTRS) != 0;
+    // chunking bounds the overflow list and the staging buffers in host mode
+    const long long chunk = devptr ? std::max(1LL, n_rows) : std::max(1LL, std::min(n_rows, (256LL << 20) / row_bytes));
+    MP_CUDA(prepare(I, argmin, chunk));
+    const int nb = I->main.ctas + I->wide.ctas;
+    if (argmin) {
+        k_init_best<<<std::max(1, (nb + 255) / 256), 256, 0, s>>>(best_ms_arr(I), best_row_arr(I), nb);
+        ++g_mp_launches;
+        MP_CUDA(cudaGetLastError());
+    }
+    if (n_rows > 0) {
+        if (devptr) {
+            MP_CUDA(run_rows(I, rows, n_rows, 0, 0, n_rows * row_bytes, makespan, status, mem_dev,
+                             reinterpret_cast<long long *>(overflow), argmin, s));
+        } else {
+            // host buffers: double-buffered chunks, H2D on the copy stream
+            // overlapping the evaluation of the previous chunk.
+            const size_t rb = static_cast<size_t>(chunk * row_bytes + 64);
+            const size_t ob = static_cast<size_t>(chunk) * (8 + 1 + 4 + 8) + 64;
+            for (int k = 0; k < 2; ++k) {
+                MP_CUDA(I->rows_dev[k].ensure(rb));
+                MP_CUDA(I->out_dev[k].ensure(ob));
+            }
+            const long long nchunks = (n_rows + chunk - 1) / chunk;
+            MP_CUDA(cudaEventRecord(I->ev_used[0], s));
+            MP_CUDA(cudaEventRecord(I->ev_used[1], s));
+            for (long long c = 0; c < nchunks; ++c) {
+                const int k = static_cast<int>(c & 1);
+                const long long r0 = c * chunk;
+                const long long nr = std::min(chunk, n_rows - r0);
+                unsigned char *drows = static_cast<unsigned char *>(I->rows_dev[k].p);
+                MP_CUDA(cudaStreamWaitEvent(I->copy_stream, I->ev_used[k], 0));
+                // pinned sources overlap with the previous chunk's kernel; pageable
+                // ones are staged by the driver (still correct, less overlap)
+                MP_CUDA(cudaMemcpyAsync(drows, rows + r0 * row_bytes, static_cast<size_t>(nr * row_bytes),
+                                        cudaMemcpyHostToDevice, I->copy_stream));
+                MP_CUDA(cudaEventRecord(I->ev_copy[k], I->copy_stream));
+                MP_CUDA(cudaStreamWaitEvent(s, I->ev_copy[k], 0));
+                unsigned char *o = static_cast<unsigned char *>(I->out_dev[k].p);
+                double *dms = makespan ? reinterpret_cast<double *>(o) : nullptr;
+                long long *dov = overflow ? reinterpret_cast<long long *>(o + 8 * chunk) : nullptr;
+                int32_t *dmd = mem_dev ? reinterpret_cast<int32_t *>(o + 16 * chunk) : nullptr;
+                int8_t *dst = status ? reinterpret_cast<int8_t *>(o + 20 * chunk) : nullptr;
+                MP_CUDA(run_rows(I, drows, nr, r0, r0, nr * row_bytes, dms, dst, dmd, dov, argmin, s));
+                if (makespan) MP_CUDA(cudaMemcpyAsync(makespan + r0, dms, 8 * nr, cudaMemcpyDeviceToHost, s));
+                if (overflow) MP_CUDA(cudaMemcpyAsync(overflow + r0, dov, 8 * nr, cudaMemcpyDeviceToHost, s));
+                if (mem_dev) MP_CUDA(cudaMemcpyAsync(mem_dev + r0, dmd, 4 * nr, cudaMemcpyDeviceToHost, s));
+                if (status) MP_CUDA(cudaMemcpyAsync(status + r0, dst, nr, cudaMemcpyDeviceToHost, s));
+                MP_CUDA(cudaEventRecord(I->ev_used[k], s));
+            }
+        }
+    }
+    if (argmin) {
+        double *dres_ms = reinterpret_cast<double *>(static_cast<unsigned char *>(I->cta_best.p) +
+                                                     static_cast<size_t>(nb) * 16);
+        long long *dres_row = reinterpret_cast<long long *>(dres_ms + 1);
+        MP_CUDA(mp_launch_finalize(best_ms_arr(I), best_row_arr(I), nb, dres_ms, dres_row, s));
+        double hm = 0;
+        long long hr = -1;
+        MP_CUDA(cudaMemcpyAsync(&hm, dres_ms, 8, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaMemcpyAsync(&hr, dres_row, 8, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        if (best_ms) *best_ms = hm;
+        if (best_row) *best_row = hr;
+    } else if (!devptr) {
+        MP_CUDA(cudaStreamSynchronize(s));
+    }
+    return MP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t mp_evaluate_batch(mp_instance *I, const uint8_t *placements, int64_t n_rows, double *makespan,
+                          int8_t *status, int32_t *mem_dev, int64_t *overflow, uint32_t flags, void *stream,
+                          mp_error *err) {
+    return evaluate_impl(I, placements, n_rows, makespan, status, mem_dev, overflow, false, nullptr, nullptr,
+                         flags, stream, err);
+}
+
+int32_t mp_evaluate_argmin(mp_instance *I, const uint8_t *placements, int64_t n_rows, double *makespan,
+                           int8_t *status, int64_t *best_row, double *best_ms, uint32_t flags, void *stream,
+                           mp_error *err) {
+    return evaluate_impl(I, placements, n_rows, makespan, status, nullptr, nullptr, true, best_row, best_ms, flags,
+                         stream, err);
+}
+
+int32_t mp_enumerate_argmin(mp_instance *I, const int32_t *op_order, uint64_t first, uint64_t count,
+                            int64_t *best_index, double *best_ms, void *stream, mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!I || !op_order) return set_err(err, MP_ERR_INVALID, 0, 0, "null argument");
+    const int n = I->n_ops, K = I->K;
+    if (static_cast<double>(n) * std::log2(static_cast<double>(K)) > 24.0)
+        return set_err(err, MP_ERR_TOO_LARGE, n, K, "%d^%d assignments exceed the enumeration guard", K, n);
+    unsigned long long total = 1;
+    for (int i = 0; i < n; ++i) total *= static_cast<unsigned long long>(K);
+    if (first > total || count > total - first) return set_err(err, MP_ERR_INVALID, first, count, "range out of bounds");
+    std::lock_guard<std::mutex> lk(I->mu);
+    MP_CUDA(cudaSetDevice(I->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : I->stream;
+    // digit t of index x is (x / K^(n-1-t)) % K and goes to op op_order[t] (solver.py:271-272)
+    std::vector<unsigned long long> pw(n);
+    std::vector<uint32_t> ord(n);
+    std::vector<char> seen(n, 0);
+    for (int t = 0; t < n; ++t) {
+        const int o = op_order[t];
+        if (o < 0 || o >= n || seen[o]) return set_err(err, MP_ERR_INVALID, t, o, "op_order is not a permutation");
+        seen[o] = 1;
+        ord[t] = static_cast<uint32_t>(o);
+        unsigned long long w = 1;
+        for (int u = 0; u < n - 1 - t; ++u) w *= static_cast<unsigned long long>(K);
+        pw[t] = w;
+    }
+    MP_CUDA(I->small.ensure(16ULL * n + 64));
+    unsigned long long *dpw = static_cast<unsigned long long *>(I->small.p);
+    uint32_t *dord = reinterpret_cast<uint32_t *>(dpw + n);
+    MP_CUDA(cudaMemcpyAsync(dpw, pw.data(), 8ULL * n, cudaMemcpyHostToDevice, s));
+    MP_CUDA(cudaMemcpyAsync(dord, ord.data(), 4ULL * n, cudaMemcpyHostToDevice, s));
+    // the main variant is exact for enumeration when its ready capacity covers
+    // every node (always the case off-chip); otherwise use the off-chip variant
+    const bool use_main = I->main_rcap >= I->ready_bound;
+    MP_CUDA(prepare(I, true, 1));
+    if (!use_main) {
+        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes));
+    }
+    const int nb = I->main.ctas + I->wide.ctas;
+    k_init_best<<<std::max(1, (nb + 255) / 256), 256, 0, s>>>(best_ms_arr(I), best_row_arr(I), nb);
+    ++g_mp_launches;
+    unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
+    MP_CUDA(cudaMemsetAsync(ctr, 0, 64, s));
+    EvalArgs a = base_args(I, !use_main);
+    a.n_rows = static_cast<long long>(count);
+    a.enum_first = first;
+    a.enum_order = dord;
+    a.enum_pow = dpw;
+    a.cta_best_ms = best_ms_arr(I);
+    a.cta_best_row = best_row_arr(I);
+    a.want_argmin = 1;
+    a.next = ctr;
+    a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
+    MP_CUDA(I->ovf_rows.ensure(64));
+    a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    MP_CUDA(mp_launch_eval(use_main ? I->main : I->wide, SRC_ENUM, false, a, s));
+    double *dres_ms = reinterpret_cast<double *>(static_cast<unsigned char *>(I->cta_best.p) + static_cast<size_t>(nb) * 16);
+    long long *dres_row = reinterpret_cast<long long *>(dres_ms + 1);
+    MP_CUDA(mp_launch_finalize(best_ms_arr(I), best_row_arr(I), nb, dres_ms, dres_row, s));
+    double hm = 0;
+    long long hr = -1;
+    MP_CUDA(cudaMemcpyAsync(&hm, dres_ms, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&hr, dres_row, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (best_ms) *best_ms = hm;
+    if (best_index) *best_index = hr;
+    return MP_OK;
+}
+
+int32_t mp_schedule_one(mp_instance *I, const uint8_t *placement, double *starts, double *ends, double *makespan,
+                        mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!I || !placement) return set_err(err, MP_ERR_INVALID, 0, 0, "null argument");
+    std::lock_guard<std::mutex> lk(I->mu);
+    MP_CUDA(cudaSetDevice(I->device));
+    cudaStream_t s = I->stream;
+    const int n = I->n_ops, N = I->n_nodes;
+    MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide_so.bytes)));
+    const size_t need = align16(n + 16) + 16ULL * N + 64 + 64;
+    MP_CUDA(I->small.ensure(need));
+    unsigned char *base = static_cast<unsigned char *>(I->small.p);
+    uint8_t *drow = base;
+    double *dst = reinterpret_cast<double *>(base + align16(n + 16));
+    double *den = dst + N;
+    double *dms = den + N;
+    int8_t *dstat = reinterpret_cast<int8_t *>(dms + 1);
+    int32_t *dmd = reinterpret_cast<int32_t *>(dms + 2);
+    long long *dov = reinterpret_cast<long long *>(dms + 3);
+    MP_CUDA(I->ctrs.ensure(64));
+    MP_CUDA(I->ovf_rows.ensure(64));
+    unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
+    MP_CUDA(cudaMemsetAsync(ctr, 0, 64, s));
+    MP_CUDA(cudaMemcpyAsync(drow, placement, n, cudaMemcpyHostToDevice, s));
+    EvalArgs a = base_args(I, true);
+    a.rows = drow;
+    a.n_rows = 1;
+    a.rows_bytes = n;
+    a.makespan = dms;
+    a.status = dstat;
+    a.mem_dev = dmd;
+    a.overflow = dov;
+    a.starts = dst;
+    a.ends = den;
+    a.next = ctr;
+    a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
+    a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    a.want_argmin = 0;
+    LaunchShape one = I->wide;
+    one.ctas = 1;
+    one.threads = 32;
+    one.groups_per_cta = 1;
+    a.groups_per_cta = 1;
+    MP_CUDA(mp_launch_eval(one, SRC_LOAD, true, a, s));
+    double hms = 0;
+    int8_t hst = 0;
+    int32_t hmd = 0;
+    long long hov = 0;
+    MP_CUDA(cudaMemcpyAsync(&hms, dms, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&hst, dstat, 1, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&hmd, dmd, 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&hov, dov, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (hst == MP_ROW_BAD_DEVICE) return set_err(err, MP_ERR_BAD_DEVICE, 0, 0, "placement names an unknown device");
+    if (hst == MP_ROW_MEMORY)
+        return set_err(err, MP_ERR_MEMORY_EXCEEDED, hmd, hov, "device index %d over capacity by %lld bytes", hmd, hov);
+    if (starts) MP_CUDA(cudaMemcpy(starts, dst, 8ULL * N, cudaMemcpyDeviceToHost));
+    if (ends) MP_CUDA(cudaMemcpy(ends, den, 8ULL * N, cudaMemcpyDeviceToHost));
+    if (makespan) *makespan = hms;
+    return MP_OK;
+}
+
+}  // extern "C"
+
+extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int32_t n_seed, int64_t n_chains,
+                                   int64_t chain_base, int32_t moves, uint64_t rng_seed, uint8_t *best_row,
+                                   double *best_ms, int64_t *best_chain, double *chain_ms, void *stream,
+                                   mp_error *err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (!I || !seed_rows || n_seed <= 0 || n_chains <= 0 || moves < 0 || chain_base < 0)
+        return set_err(err, MP_ERR_INVALID, n_seed, n_chains, "bad local-search arguments");
+    std::lock_guard<std::mutex> lk(I->mu);
+    MP_CUDA(cudaSetDevice(I->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : I->stream;
+    const int n = I->n_ops;
+    for (long long r = 0; r < static_cast<long long>(n_seed) * n; ++r)
+        if (seed_rows[r] >= I->K) return set_err(err, MP_ERR_BAD_DEVICE, r / n, seed_rows[r], "seed row names an unknown device");
+    // an exact evaluation needs a ready capacity that covers the bound on-chip
+    const bool onchip = I->main.onchip && I->main_rcap >= I->ready_bound;
+    if (!I->main.onchip) {
+        MP_CUDA(I->main_state.ensure(static_cast<size_t>(I->main.ctas) * I->main.groups_per_cta * I->main_so.bytes));
+    } else if (!onchip) {
+        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes));
+    }
+    const size_t seed_b = align16(static_cast<size_t>(n_seed) * n);
+    const size_t rows_b = align16(static_cast<size_t>(n_chains) * n);
+    DevBuf buf;
+    MP_CUDA(buf.ensure(seed_b + rows_b + 8ULL * n_chains + 64));
+    unsigned char *base = static_cast<unsigned char *>(buf.p);
+    uint8_t *dseed = base;
+    uint8_t *drows = base + seed_b;
+    double *dms = reinterpret_cast<double *>(base + seed_b + rows_b);
+    double *dbest = dms + n_chains;
+    long long *dbc = reinterpret_cast<long long *>(dbest + 1);
+    MP_CUDA(cudaMemcpyAsync(dseed, seed_rows, static_cast<size_t>(n_seed) * n, cudaMemcpyHostToDevice, s));
+    MP_CUDA(I->ctrs.ensure(64));
+    MP_CUDA(I->ovf_rows.ensure(64));
+    unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
+    MP_CUDA(cudaMemsetAsync(ctr, 0, 64, s));
+    const bool use_wide = I->main.onchip && !onchip;
+    EvalArgs a = base_args(I, use_wide);
+    a.next = ctr;
+    a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
+    a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    LsArgs ls{};
+    ls.seed_rows = dseed;
+    ls.n_seed = n_seed;
+    ls.n_chains = n_chains;
+    ls.chain_base = chain_base;
+    ls.moves = moves;
+    ls.rng_seed = rng_seed;
+    ls.chain_rows = drows;
+    ls.chain_ms = dms;
+    MP_CUDA(mp_launch_ls(use_wide ? I->wide : I->main, a, ls, s));
+    MP_CUDA(mp_launch_ls_pick(dms, n_chains, dbest, dbc, s));
+    double hms = 0;
+    long long hc = -1;
+    MP_CUDA(cudaMemcpyAsync(&hms, dbest, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&hc, dbc, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (hc >= 0 && best_row) MP_CUDA(cudaMemcpy(best_row, drows + static_cast<size_t>(hc) * n, n, cudaMemcpyDeviceToHost));
+    if (chain_ms) MP_CUDA(cudaMemcpy(chain_ms, dms, 8ULL * n_chains, cudaMemcpyDeviceToHost));
+    if (best_ms) *best_ms = hms;
+    if (best_chain) *best_chain = hc >= 0 ? hc + chain_base : -1;
+    return MP_OK;
+}

@@ -1,0 +1,231 @@
+"""Fusion rules and GCOF coarsening (``pkg/src/opplace/fusion.py``).
+
+Rule types and the single-pair helpers (``match_rule``, ``classify_connection``,
+``is_valid_conn``) are small host utilities of the API.  :func:`gcof` — the hot
+path — runs on the GPU through ``mp_coarsen`` (K1/K2, csrc/mp_coarsen.cu): the
+graph, the interned type sequences and the rules are flattened here, the
+partition, fused costs and quotient edges come back as arrays, and the output
+``CompGraph`` is assembled from them (singleton groups reuse the input node
+objects exactly as ``materialize`` does, ``fusion.py:233-235``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from dataclasses import dataclass
+from enum import Enum
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from . import _native as N
+from .errors import CycleError, UnknownEdgeError
+from .graph import CompGraph, FlowEdge, OpNode, Tag, find_cycle
+from .profiles import CostOverrides
+
+FUSE_JOINER = "∘"  # joins member types in a fused node's op_type (fusion.py:23)
+
+
+class ConnKind(Enum):
+    DIRECT = "direct"
+    MULTI_OUTPUTS = "multi_outputs"
+    MULTI_INPUTS = "multi_inputs"
+
+
+@dataclass(frozen=True)
+class FusionRule:
+    """A type sequence that may become one kernel (``fusion.py:32-43``)."""
+
+    id: int
+    pattern: tuple[str, ...]
+
+    def __post_init__(self):
+        if len(self.pattern) < 2:
+            raise ValueError(f"rule {self.id}: pattern needs at least two op types")
+        if not all(self.pattern):
+            raise ValueError(f"rule {self.id}: empty op type in pattern")
+
+
+class FusionRuleSet:
+    """Rules with unique ids (``fusion.py:46-63``)."""
+
+    def __init__(self, rules: Iterable[FusionRule]):
+        self.rules = list(rules)
+        ids = [r.id for r in self.rules]
+        if len(ids) != len(set(ids)):
+            raise ValueError("duplicate rule ids")
+        self._patterns = frozenset(r.pattern for r in self.rules)
+
+    def has_pattern(self, seq: tuple[str, ...]) -> bool:
+        return seq in self._patterns
+
+    def __iter__(self) -> Iterator[FusionRule]:
+        return iter(self.rules)
+
+    def __len__(self) -> int:
+        return len(self.rules)
+
+
+class MatchKind(Enum):
+    FULL = "full"
+    PREFIX = "prefix"
+
+
+@dataclass(frozen=True)
+class Match:
+    kind: MatchKind
+    rule_id: int
+
+
+def classify_connection(g: CompGraph, src: int, dst: int) -> ConnKind:
+    """Edge class by endpoint degrees (``fusion.py:77-85``)."""
+    if g.edge(src, dst) is None:
+        raise UnknownEdgeError(src, dst)
+    if g.out_degree(src) > 1:
+        return ConnKind.MULTI_OUTPUTS
+    return ConnKind.MULTI_INPUTS if g.in_degree(dst) > 1 else ConnKind.DIRECT
+
+
+def is_valid_conn(g: CompGraph, src: int, dst: int) -> bool:
+    return classify_connection(g, src, dst) is not ConnKind.MULTI_OUTPUTS
+
+
+def match_sequences(pred_seq, succ_seq, rules: FusionRuleSet) -> Match | None:
+    """Strict-prefix matches beat full ones; lowest rule id (``fusion.py:93-104``)."""
+    t = tuple(pred_seq) + tuple(succ_seq)
+    n = len(t)
+    pref = [r.id for r in rules if len(r.pattern) > n and r.pattern[:n] == t]
+    if pref:
+        return Match(MatchKind.PREFIX, min(pref))
+    full = [r.id for r in rules if r.pattern == t]
+    return Match(MatchKind.FULL, min(full)) if full else None
+
+
+def match_rule(pred: OpNode, succ: OpNode, rules: FusionRuleSet) -> Match | None:
+    return match_sequences(pred.type_seq, succ.type_seq, rules)
+
+
+_TAG_CODE = {Tag.PLAIN: 0, Tag.FUSED: 1, Tag.BOUND: 2}
+_CODE_TAG = {0: Tag.PLAIN, 1: Tag.FUSED, 2: Tag.BOUND}
+
+
+class _Flat:
+    """Array form of a coarsening problem (mp_coarsen_input)."""
+
+    def __init__(self, g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None):
+        types: dict[str, int] = {}
+
+        def tid(t: str) -> int:
+            v = types.get(t)
+            if v is None:
+                v = types[t] = len(types)
+            return v
+
+        nodes = g.nodes
+        dg = g.csr()
+        devs = set()
+        for n in nodes:
+            devs.update(n.compute_time)
+        if overrides is not None:
+            devs.update(k for (_, k) in overrides.entries)
+        self.devices = sorted(devs)
+        dindex = {d: i for i, d in enumerate(self.devices)}
+        V, D = len(nodes), len(self.devices)
+        seq_beg = np.zeros(V + 1, np.int32)
+        seq = []
+        tag = np.empty(V, np.int32)
+        mem = np.empty(V, np.int64)
+        cost = np.full((V, max(D, 1)), np.nan)
+        for i, n in enumerate(nodes):
+            seq.extend(tid(t) for t in n.type_seq)
+            seq_beg[i + 1] = len(seq)
+            tag[i] = _TAG_CODE[n.tag]
+            mem[i] = n.mem_bytes
+            for k, t in n.compute_time.items():
+                cost[i, dindex[k]] = float(t)
+        rb = np.zeros(len(rules) + 1, np.int32)
+        rt = []
+        rid = np.empty(len(rules), np.int32)
+        for r, rule in enumerate(rules):
+            rid[r] = rule.id
+            rt.extend(tid(t) for t in rule.pattern)
+            rb[r + 1] = len(rt)
+        ob = [0]
+        ot = []
+        odev = []
+        otime = []
+        if overrides is not None:
+            for (s, k), t in overrides.entries.items():
+                ot.extend(tid(x) for x in s)
+                ob.append(len(ot))
+                odev.append(dindex[k])
+                otime.append(float(t))
+        self.keep = [
+            dg.ids, seq_beg, np.asarray(seq or [0], np.int32), tag, mem, np.ascontiguousarray(cost),
+            dg.esrc, dg.edst, dg.payload, rid, rb, np.asarray(rt or [0], np.int32),
+            np.asarray(ob, np.int32), np.asarray(ot or [0], np.int32), np.asarray(odev or [0], np.int32),
+            np.asarray(otime or [0.0], np.float64),
+        ]
+        k = self.keep
+        self.cin = N.mp_coarsen_input(
+            V, len(dg.esrc), max(D, 1), N.ptr(k[0]), N.ptr(k[1]), N.ptr(k[2]), N.ptr(k[3]), N.ptr(k[4]),
+            N.ptr(k[5]), N.ptr(k[6]), N.ptr(k[7]), N.ptr(k[8]), len(rules), N.ptr(k[9]), N.ptr(k[10]),
+            N.ptr(k[11]), len(otime), N.ptr(k[12]), N.ptr(k[13]), N.ptr(k[14]), N.ptr(k[15]),
+            1 if sys.version_info >= (3, 12) else 0)
+
+
+def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = None,
+         device: int = 0) -> CompGraph:
+    """GCOF coarsening on the GPU (``fusion.py:271-304``).
+
+    Same output as the reference, node by node (ids, op types, members, type
+    sequences, tags, memory, fp64 costs bit for bit) and edge list order
+    (sorted by ``(u, v)``); ``CycleError`` on cyclic input.
+    """
+    if len(g) == 0:
+        return CompGraph([], [])
+    flat = _Flat(g, rules, overrides)
+    out = N.mp_coarsen_output()
+    err = N.mp_error()
+    lib = N.lib()
+    code = lib.mp_coarsen(C.byref(flat.cin), device, C.byref(out), C.byref(err))
+    if code == N.MP_ERR_CYCLE:
+        ids = g.node_ids
+        raise CycleError(find_cycle(ids, {i: g.succs(i) for i in ids}))
+    N.check(code, err, "mp_coarsen")
+    try:
+        nodes_in = g.nodes
+        ng, ne = out.n_groups, out.n_edges
+        D = len(flat.devices)
+        grp_node = np.ctypeslib.as_array(out.grp_node, (ng,)).copy() if ng else np.zeros(0, np.int32)
+        grp_tag = np.ctypeslib.as_array(out.grp_tag, (ng,)).copy() if ng else np.zeros(0, np.int32)
+        mbeg = np.ctypeslib.as_array(out.mem_beg, (ng + 1,)).copy()
+        members = np.ctypeslib.as_array(out.members, (int(mbeg[-1]),)).copy() if mbeg[-1] else np.zeros(0, np.int32)
+        gmem = np.ctypeslib.as_array(out.grp_mem, (ng,)).copy() if ng else np.zeros(0, np.int64)
+        gcost = (np.ctypeslib.as_array(out.grp_cost, (ng * max(D, 1),)).reshape(ng, max(D, 1)).copy()
+                 if ng else np.zeros((0, 1)))
+        esrc = np.ctypeslib.as_array(out.out_src, (ne,)).copy() if ne else np.zeros(0, np.int32)
+        edst = np.ctypeslib.as_array(out.out_dst, (ne,)).copy() if ne else np.zeros(0, np.int32)
+        epay = np.ctypeslib.as_array(out.out_payload, (ne,)).copy() if ne else np.zeros(0, np.int64)
+    finally:
+        lib.mp_coarsen_free(C.byref(out))
+    new_nodes = []
+    gid_of = []
+    for z in range(ng):
+        mem_idx = members[mbeg[z]:mbeg[z + 1]]
+        if len(mem_idx) == 1:
+            n = nodes_in[int(mem_idx[0])]
+            new_nodes.append(n)
+            gid_of.append(n.id)
+            continue
+        parts = [nodes_in[int(m)] for m in mem_idx]
+        seq = tuple(t for p in parts for t in p.type_seq)
+        mids = tuple(x for p in parts for x in p.members)
+        cost = {flat.devices[k]: float(gcost[z, k]) for k in range(D) if not np.isnan(gcost[z, k])}
+        gid = min(p.id for p in parts)
+        new_nodes.append(OpNode(gid, FUSE_JOINER.join(seq), int(gmem[z]), cost, mids, seq,
+                                _CODE_TAG[int(grp_tag[z])]))
+        gid_of.append(gid)
+    edges = [FlowEdge(gid_of[int(u)], gid_of[int(v)], int(p)) for u, v, p in zip(esrc, edst, epay)]
+    return CompGraph(new_nodes, edges)

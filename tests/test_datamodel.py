@@ -1,0 +1,183 @@
+"""Host data model of the drop-in surface, mirroring the reference's own tests
+(pkg/tests/test_graph.py, test_profiles.py, test_fusion.py helpers)."""
+
+from __future__ import annotations
+
+import itertools
+import logging
+import random
+
+import pytest
+
+import paper_2312_04025_b200 as mp
+from paper_2312_04025_b200 import workloads
+
+
+def _node(i, t="conv", **kw):
+    return mp.OpNode(i, t, kw.pop("mem", 1), kw.pop("times", {0: 1.0}), **kw)
+
+
+def diamond():
+    return mp.CompGraph([_node(i) for i in (1, 2, 3, 4)],
+                        [mp.FlowEdge(1, 2, 5), mp.FlowEdge(1, 3, 6), mp.FlowEdge(2, 4, 7), mp.FlowEdge(3, 4, 8)])
+
+
+def test_opnode_and_edge_validation():
+    n = _node(3)
+    assert n.members == (3,) and n.type_seq == ("conv",) and n.tag is mp.Tag.PLAIN
+    with pytest.raises(ValueError):
+        mp.OpNode(1, "x", -1, {})
+    with pytest.raises(ValueError):
+        mp.OpNode(1, "x", 1, {0: -1.0})
+    with pytest.raises(ValueError):
+        mp.OpNode(1, "x", 1, {}, members=(1, 1), type_seq=("a", "b"))
+    with pytest.raises(ValueError):
+        mp.OpNode(1, "x", 1, {}, members=(1, 2), type_seq=("a",))
+    with pytest.raises(ValueError):
+        mp.FlowEdge(1, 1, 0)
+    with pytest.raises(ValueError):
+        mp.FlowEdge(1, 2, -5)
+
+
+def test_compgraph_contract():
+    with pytest.raises(ValueError):
+        mp.CompGraph([_node(1), _node(1)], [])
+    with pytest.raises(mp.DanglingEdgeError):
+        mp.CompGraph([_node(1)], [mp.FlowEdge(1, 2, 1)])
+    with pytest.raises(ValueError):
+        mp.CompGraph([_node(1), _node(2)], [mp.FlowEdge(1, 2, 1), mp.FlowEdge(1, 2, 3)])
+    g = mp.CompGraph([_node(3), _node(1), _node(2)], [mp.FlowEdge(3, 1, 1), mp.FlowEdge(1, 2, 1),
+                                                       mp.FlowEdge(3, 2, 9)])
+    assert g.node_ids == [1, 2, 3]
+    assert [(e.src, e.dst) for e in g.edges] == [(3, 1), (1, 2), (3, 2)]  # insertion order
+    assert g.succs(3) == [1, 2] and g.preds(2) == [1, 3]
+    assert g.edge(3, 2).payload_bytes == 9 and g.edge(2, 3) is None
+    assert g == mp.CompGraph(list(g.nodes), list(reversed(g.edges)))
+    dg = g.csr()
+    assert list(dg.esrc) == [2, 0, 2] and list(dg.edst) == [0, 1, 1]
+
+
+def test_validate_and_topo():
+    g = diamond()
+    mp.validate_dag(g)
+    assert mp.topo_order(g) == [1, 2, 3, 4]
+    cyc = mp.CompGraph([_node(1), _node(2), _node(3)],
+                       [mp.FlowEdge(1, 2, 1), mp.FlowEdge(2, 3, 1), mp.FlowEdge(3, 2, 1)])
+    with pytest.raises(mp.CycleError) as ei:
+        mp.validate_dag(cyc)
+    assert ei.value.cycle == [3, 2]  # same witness as the reference (graph.py:234-264)
+    with pytest.raises(mp.CycleError):
+        mp.topo_order(cyc)
+
+
+def test_validate_warns_on_disconnected(caplog):
+    g = mp.CompGraph([_node(1), _node(2)], [])
+    with caplog.at_level(logging.WARNING):
+        mp.validate_dag(g)
+    assert "not weakly connected" in caplog.text
+
+
+def test_augment_ids_follow_edge_order():
+    g = mp.CompGraph([_node(5), _node(7), _node(9)], [mp.FlowEdge(9, 5, 1), mp.FlowEdge(5, 7, 2)])
+    aug = mp.augment(g)
+    assert aug.flow_ids == [10, 11]
+    assert aug.flow_nodes[10].src == 9 and aug.flow_nodes[11].dst == 7
+    assert aug.succs(9) == [10] and aug.preds(5) == [10]
+    assert mp.contract(aug) == g
+
+
+def test_succ_closure():
+    c = mp.succ_closure(diamond())
+    assert c[1] == frozenset({2, 3, 4}) and c[4] == frozenset()
+
+
+def _widest_by_paths(c, src, dst):
+    best = 0.0
+    others = [d for d in c.device_ids if d not in (src, dst)]
+    for r in range(len(others) + 1):
+        for mids in itertools.permutations(others, r):
+            path = (src, *mids, dst)
+            w = min(c.links.get((a, b), 0.0) for a, b in zip(path, path[1:]))
+            best = max(best, w)
+    return best
+
+
+def test_effective_bandwidth_is_the_widest_path():
+    for trial in range(40):
+        rng = random.Random(trial)
+        n = rng.randint(2, 5)
+        ids = list(range(1, n + 1))
+        links = {(a, b): float(rng.randint(1, 40)) * 1e6 for a in ids for b in ids if a != b and rng.random() < 0.7}
+        for a, b in zip(ids, ids[1:] + ids[:1]):
+            links.setdefault((a, b), 2e6)
+            links.setdefault((b, a), 2e6)
+        c = mp.Cluster([mp.Device(i, 10) for i in ids], links)
+        mesh = mp.effective_bandwidth(c)
+        for a in ids:
+            for b in ids:
+                if a != b:
+                    assert mesh.bandwidth(a, b) == _widest_by_paths(c, a, b)
+
+
+def test_cluster_errors_and_comm_time():
+    with pytest.raises(ValueError):
+        mp.Device(1, 0)
+    with pytest.raises(mp.DisconnectedClusterError):
+        mp.Cluster([mp.Device(1, 10), mp.Device(2, 10)], {})
+    with pytest.raises(mp.DisconnectedClusterError):
+        mp.effective_bandwidth(mp.Cluster([mp.Device(1, 10), mp.Device(2, 10)], {(1, 2): 1e6}))
+    relay = mp.Cluster([mp.Device(1, 100), mp.Device(2, 100), mp.Device(3, 100)],
+                       {(1, 2): 1e7, (2, 1): 1e7, (2, 3): 5e6, (3, 2): 5e6})
+    mesh = mp.effective_bandwidth(relay)
+    assert mp.comm_time(100_000_000, 1, 3, mesh) == 20.0  # test_acceptance.py:113-118
+    assert mp.comm_time(5, 2, 2, mesh) == 0.0
+
+
+def test_fused_cost_and_overrides():
+    n = mp.OpNode(1, "conv∘bn", 1, {0: 5.0}, members=(1, 2), type_seq=("conv", "bn"), tag=mp.Tag.FUSED)
+    ov = mp.CostOverrides({(("conv", "bn"), 0): 3.5})
+    assert mp.fused_cost(n, 0, ov) == 3.5 and mp.fused_cost(n, 0) == 5.0
+    with pytest.raises(mp.MissingProfileError):
+        mp.fused_cost(n, 1)
+    with pytest.raises(ValueError):
+        mp.CostOverrides({(("a",), 0): -1.0})
+
+
+def test_rules_and_matching():
+    rules = workloads.table_rules()
+    assert rules.has_pattern(("conv", "bn")) and not rules.has_pattern(("bn", "conv"))
+    with pytest.raises(ValueError):
+        mp.FusionRule(1, ("a",))
+    with pytest.raises(ValueError):
+        mp.FusionRuleSet([mp.FusionRule(1, ("a", "b")), mp.FusionRule(1, ("c", "d"))])
+    assert mp.match_rule(_node(1, "conv"), _node(2, "bn"), rules) == mp.Match(mp.MatchKind.PREFIX, 2)
+    pair = mp.OpNode(1, "conv∘bn", 2, {0: 2.0}, members=(1, 2), type_seq=("conv", "bn"), tag=mp.Tag.BOUND)
+    assert mp.match_rule(pair, _node(3, "relu"), rules) == mp.Match(mp.MatchKind.FULL, 2)
+    assert mp.match_rule(_node(1, "bn"), _node(2, "conv"), rules) is None
+
+
+def test_connection_classes():
+    g = mp.CompGraph([_node(1), _node(2, "bn"), _node(3, "relu"), _node(4, "add")],
+                     [mp.FlowEdge(1, 2, 1), mp.FlowEdge(1, 3, 1), mp.FlowEdge(2, 4, 1), mp.FlowEdge(3, 4, 1)])
+    assert mp.classify_connection(g, 1, 2) is mp.ConnKind.MULTI_OUTPUTS
+    assert mp.classify_connection(g, 2, 4) is mp.ConnKind.MULTI_INPUTS
+    assert not mp.is_valid_conn(g, 1, 3) and mp.is_valid_conn(g, 3, 4)
+    with pytest.raises(mp.UnknownEdgeError):
+        mp.classify_connection(g, 2, 3)
+
+
+def test_solve_budget_validation():
+    with pytest.raises(ValueError):
+        mp.SolveBudget(gap=1.0)
+    assert mp.SolveBudget().gap == 0.0
+
+
+def test_public_surface_names():
+    """Every hot-path name of the reference surface exists (opplace/__init__.py:94-112)."""
+    for name in ("AugGraph", "Cluster", "CompGraph", "CostOverrides", "CycleError", "Device", "EffectiveMesh",
+                 "Event", "EventKind", "FlowEdge", "FlowNode", "FusionRule", "FusionRuleSet", "GenSpec",
+                 "MemoryExceededError", "MissingCostError", "OpNode", "Schedule", "Solution", "SolveBudget",
+                 "Status", "Tag", "TooLargeError", "augment", "brute_force", "comm_time", "effective_bandwidth",
+                 "fused_cost", "gcof", "gen_synthetic", "match_rule", "schedule_for_assignment", "simulate",
+                 "solve_exact", "topo_order", "validate_dag"):
+        assert hasattr(mp, name), name

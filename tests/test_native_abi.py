@@ -1,0 +1,72 @@
+"""The C ABI library loads, exports exactly what include/moirai_b200.h declares,
+and — with no GPU visible — refuses to compute instead of falling back to CPU."""
+
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2312_04025_b200 as mp
+from paper_2312_04025_b200 import _native as N
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "moirai_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mp_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declares_what_the_binding_types():
+    assert declared_symbols() == sorted(N.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(str(N.LIB_PATH))
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.mp_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    # spot-check sizes against the header's field lists
+    assert C.sizeof(N.mp_error) == 8 + 8 + 8 + 200  # int32 padded to 8, two int64, char[200]
+    assert C.sizeof(N.mp_problem) == 16 + 7 * 8
+    assert C.sizeof(N.mp_instance_info) == 12 * 4 + 2 * 8
+
+
+def _no_gpu():
+    return N.lib().mp_device_count() == 0
+
+
+@pytest.mark.skipif(not _no_gpu(), reason="only meaningful where no GPU is visible")
+def test_no_cpu_fallback_without_gpu():
+    g = mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0, 1: 2.0})], [])
+    c = mp.Cluster([mp.Device(0, 10), mp.Device(1, 10)], {(0, 1): 1e6, (1, 0): 1e6})
+    with pytest.raises(mp.NativeError):
+        mp.schedule_for_assignment(g, c, mp.effective_bandwidth(c), {1: 0})
+    with pytest.raises(mp.NativeError):
+        mp.gcof(g, mp.FusionRuleSet([]))
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(mp.NativeError):
+        N.load_library(tmp_path / "nope.so")
+
+
+def test_validation_before_the_gpu():
+    """Errors the reference raises before any scheduling are raised host-side
+    in the same order (solver.py:46-55)."""
+    c = mp.Cluster([mp.Device(0, 10), mp.Device(1, 10)], {(0, 1): 1e6, (1, 0): 1e6})
+    mesh = mp.effective_bandwidth(c)
+    with pytest.raises(ValueError):
+        mp.Instance(mp.CompGraph([], []), c, mesh)
+    with pytest.raises(mp.MissingCostError) as ei:
+        mp.Instance(mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0})], []), c, mesh)
+    assert (ei.value.op, ei.value.device) == (1, 1)
+    assert np.isnan(np.nan)
