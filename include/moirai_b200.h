@@ -93,6 +93,10 @@ typedef struct mp_instance_info {
     int32_t smem_bytes;         /* dynamic shared memory per CTA                     */
     int32_t onchip;             /* 1: tables + state in shared memory, 0: global     */
     int32_t device;
+    int32_t n_multi;            /* ops with >= 2 in-flows (est/npred state kept)     */
+    int32_t ready_bound;        /* path-cover bound on any ready set                 */
+    int32_t colo;               /* 1: co-located flows are not dispatched (exact: all durations > 0) */
+    int32_t colo_ok;            /* 1: the instance qualifies for colo                */
     int64_t table_bytes;        /* instance tables staged per CTA                    */
     int64_t state_bytes;        /* per-placement dynamic state                       */
 } mp_instance_info;
@@ -108,8 +112,12 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device,
                            mp_instance **out, mp_error *err);
 void    mp_instance_destroy(mp_instance *inst);
 int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
-/* Override the launch shape (lanes per placement G in {4,8,16,32}; 0 = auto). */
-int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t ctas_per_sm);
+/* Override the launch shape: lanes per placement G in {2,4,8,16,32} (0 = auto),
+ * CTAs per SM cap (0 = auto), on-chip ready capacity (0 = auto); flags bit 0
+ * (MP_TUNE_NO_COLO) dispatches co-located flows as ordinary steps. */
+#define MP_TUNE_NO_COLO 1
+int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t ctas_per_sm,
+                         int32_t ready_cap, uint32_t flags);
 
 /* ---- batched evaluation (K3; replaces one `_schedule` call per row) ------ */
 /* makespan[p] = +inf unless status[p] == MP_ROW_OK.  mem_dev/overflow may be NULL. */

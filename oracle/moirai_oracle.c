@@ -144,6 +144,10 @@ static void ws_free(orc_ws *w) {
  * One evaluation (solver.py:80-148).  Returns 0 ok, 1 memory exceeded
  * (*mem_dev, *overflow set), 2 device index out of range.
  */
+/* diagnostic only: largest ready set of the last single-threaded schedule */
+static int g_last_max_ready = 0;
+int orc_last_max_ready(void) { return g_last_max_ready; }
+
 static int schedule_ws(const orc_inst *I, orc_ws *w, const uint8_t *row, double *starts, double *ends,
                        double *makespan, int *mem_dev, int64_t *overflow) {
     const orc_problem *p = &I->p;
@@ -203,7 +207,9 @@ static int schedule_ws(const orc_inst *I, orc_ws *w, const uint8_t *row, double 
     for (int k = 0; k < 3 * K; ++k) w->op_free[k] = 0.0;
     double ms = 0.0;
     int have_ms = 0;
+    int peak = nr;
     for (int step = 0; step < N && nr > 0; ++step) {
+        if (nr > peak) peak = nr;
         int bi = -1;
         double be = 0.0, br = 0.0;
         int bn = 0;
@@ -267,6 +273,7 @@ static int schedule_ws(const orc_inst *I, orc_ws *w, const uint8_t *row, double 
         }
     }
     *makespan = ms;
+    g_last_max_ready = peak;
     return 0;
 }
 

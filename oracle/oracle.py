@@ -57,6 +57,7 @@ def lib():
         L.orc_eval_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
         L.orc_enumerate.restype = C.c_int64
         L.orc_enumerate.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+        L.orc_last_max_ready.restype = C.c_int
         L.orc_gcof.restype = C.c_int
         L.orc_gcof.argtypes = [C.POINTER(_GcofIn), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
@@ -104,6 +105,11 @@ class OracleInstance:
         ov = C.c_int64(0)
         s = lib().orc_schedule(self._h, _p(row), _p(st), _p(en), C.byref(ms), C.byref(md), C.byref(ov))
         return s, ms.value, st, en, md.value, ov.value
+
+    def max_ready(self, row) -> int:
+        """Largest ready set while scheduling `row` (diagnostic)."""
+        self.schedule(row)
+        return lib().orc_last_max_ready()
 
     def eval_batch(self, rows, threads: int = 1):
         rows = np.ascontiguousarray(rows, np.uint8)

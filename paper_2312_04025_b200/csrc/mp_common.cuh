@@ -24,32 +24,39 @@
 struct TabOff {
     uint32_t cost;      // f64 [n_ops*K]    p[i][k]                       (solver.py:61)
     uint32_t mem;       // i64 [n_ops]      mem_bytes                     (solver.py:60)
-    uint32_t payload;   // f64 [n_flows]    (double)payload_bytes         (solver.py:65,77)
     uint32_t bw;        // f64 [K*K]        effective bandwidth           (solver.py:66-67)
     uint32_t cap;       // i64 [K]          device capacity               (solver.py:59)
-    uint32_t out_beg;   // u32 [n_ops+1]    CSR: out-flows of each op
-    uint32_t out_flow;  // u32 [n_flows]    flow indices grouped by source op
-    uint32_t fsrc;      // u32 [n_flows]    source op of each flow        (solver.py:63)
-    uint32_t fdst;      // u32 [n_flows]    destination op                 (solver.py:64)
-    uint32_t indeg;     // u16 [n_ops]      in-flows per op (npred seed, solver.py:109)
+    uint32_t out_beg;   // u32 [n_ops+1]    CSR over out-flow *slots* (flows stably sorted by source)
+    uint32_t s_dst;     // u32 [n_flows]    slot -> destination op
+    uint32_t s_fid;     // u32 [n_flows]    slot -> flow index (edge order; node = n_ops + f)
+    uint32_t s_pay;     // f64 [n_flows]    slot -> (double)payload_bytes (solver.py:65,77)
+    uint32_t fdst;      // u32 [n_flows]    flow index -> destination op   (solver.py:64)
+    uint32_t mi;        // u32 [n_ops]      op -> multi-input slot, or MP_NONE (in-degree <= 1)
+    uint32_t m_op;      // u32 [n_multi]    multi-input slot -> op
+    uint32_t m_deg;     // u32 [n_multi]    multi-input slot -> in-degree (npred seed, solver.py:109)
     uint32_t lvl_ops;   // u32 [n_ops]      ops bucketed by height (0 = sinks)
     uint32_t lvl_beg;   // u32 [n_ops+1]    level offsets into lvl_ops
     uint32_t srcs;      // u32 [n_ops]      ops with no in-flow (initial ready set, solver.py:111)
     uint32_t bytes;     // total, multiple of 16
 };
 
+#define MP_NONE 0xffffffffu
+
 // Byte offsets of one placement's dynamic state ("slot") — shared memory when
 // the instance is on-chip, a per-group global scratch slice otherwise.
 struct StOff {
-    uint32_t rank;      // f64 [n_ops]   downstream critical path of each op  (solver.py:100-107)
-    uint32_t est;       // f64 [n_ops]   earliest start from finished preds   (solver.py:110,142-143)
-    uint32_t clk;       // f64 [3K+1]    op_free | out_free | in_free | 0.0   (solver.py:112-114)
-    uint32_t load;      // u64 [K]       memory load per device               (solver.py:82-84)
-    uint32_t r_est;     // f64 [rcap]    ready entries: est part of the key
-    uint32_t r_rank;    // f64 [rcap]    ready entries: rank
-    uint32_t r_meta;    // u32 [rcap]    node | clock slot 1 << 20 | clock slot 2 << 26
-    uint32_t npred;     // u16 [n_ops]   unfinished in-flows                  (solver.py:109,141)
-    uint32_t dev;       // u8  [n_ops+32] placement row (16-byte-aligned copy, see dev_off)
+    uint32_t rank;      // f64 [n_ops]    downstream critical path of each op  (solver.py:100-107)
+    uint32_t m_est;     // f64 [n_multi]  est of multi-input ops               (solver.py:110,142-143)
+    uint32_t clk;       // f64 [3K+2]     op_free | out_free | in_free | 0.0 | sink (solver.py:112-114);
+                        //                aliased by the u64 [K] memory loads before dispatch
+    uint32_t r_est;     // f64 [rcap]     ready entries: est part of the key
+    uint32_t r_rank;    // f64 [rcap]     ready entries: rank
+    uint32_t r_dur;     // f64 [rcap]     ready entries: duration (op cost or payload/bw)
+    uint32_t r_meta;    // u32 [rcap]     node | read clock slot 1 << 20 | read clock slot 2 << 26
+    uint32_t r_tie;     // u32 [rcap]     id used when e == est (co-located-flow gate)
+    uint32_t m_tie;     // u32 [n_multi]  gate id of multi-input ops
+    uint32_t m_np;      // u16 [n_multi]  unfinished in-flows                  (solver.py:109,141)
+    uint32_t dev;       // u8  [n_ops+32] placement row (16-byte-aligned copy)
     uint32_t bytes;
 };
 
@@ -57,7 +64,8 @@ struct EvalArgs {
     const unsigned char *blob;   // instance tables (global)
     TabOff to;
     StOff so;
-    int n_ops, n_flows, K, n_levels, n_src, rcap;
+    int n_ops, n_flows, K, n_levels, n_src, n_multi, rcap;
+    int colo;                     // skip co-located flows (exact when all durations > 0)
 
     // row source
     const uint8_t *rows;          // LOAD: [n_rows][n_ops]

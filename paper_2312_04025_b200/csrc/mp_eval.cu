@@ -10,20 +10,31 @@
 //      (earliest feasible start, -rank, node id)                    (:118-145)
 //   5. makespan = max end over ops                                 (:147)
 //
-// Mapping: a *group* of G lanes of one warp evaluates one
-// placement at a time; 32/G groups share a warp and all groups of a CTA share
-// the instance tables, which one thread stages into shared memory with 1-D
-// bulk-async (TMA) copies on an mbarrier.  Per-placement state (ranks, est,
-// npred, the ready set, the 3K+1 resource clocks) lives in the group's shared
-// memory slot.  The ready set is an unordered array; each dispatch step every
-// lane scans a strided slice, then a G-lane xor-butterfly reduces the
-// lexicographic key.  Flows stay implicit in the rank pass (rank of a flow =
-// its duration + the rank of its consumer), so per-placement state is O(n_ops).
+// Mapping.  A *group* of G lanes evaluates one placement; the
+// 32/G groups of a warp run in LOCKSTEP on different placements of the same
+// instance: every loop has a warp-uniform trip count and every branch is a
+// predicate, so one instruction stream advances 32/G placements.  The CTA's
+// groups share the instance tables, staged into shared memory by one thread
+// with 1-D bulk-async (TMA) copies on an mbarrier; each group's dynamic state
+// (ranks, multi-input est/npred, the ready set, 3K+2 resource clocks, the row)
+// lives in its shared-memory slot.
+//
+// Dispatch step: each lane scans a strided slice of the unordered ready array
+// for its lexicographic minimum key, a G-lane xor butterfly finds the group
+// minimum, the owning lane broadcasts the winner's duration and resource slots,
+// and the successors are appended with ballot-compacted positions.  Ready
+// entries carry their duration and the clock slots they read, so op and flow
+// commits are one code path.  Flows stay implicit in the rank pass (rank of a
+// flow = duration + rank of its consumer).
+//
+// Co-located flows (colo mode, exact when every op and crossing-flow duration
+// is > 0) are not dispatched: their consumer is updated when
+// the producer commits and carries a "tie id" that reproduces the step at
+// which the reference would have committed the zero-duration flow.
 //
 // All floating-point work is IEEE fp64 add / divide / compare, compiled with
-// --fmad=false and IEEE division, so every start, end and makespan is
-// bit-identical to the reference when the dispatch order matches — and the
-// order matches by construction (same keys, same strict tie-break).
+// --fmad=false and IEEE division: starts, ends and makespans are bit-identical
+// to the reference.
 
 #include <cfloat>
 #include <climits>
@@ -36,25 +47,26 @@ unsigned long long g_mp_launches = 0;
 namespace {
 
 constexpr double kInf = __builtin_huge_val();
+constexpr unsigned kFull = 0xffffffffu;
 
 template <int G>
-__device__ __forceinline__ unsigned group_mask(int lane) {
+__device__ __forceinline__ unsigned group_bits(int lane) {
     if constexpr (G == 32) {
-        return 0xffffffffu;
+        return kFull;
     } else {
         return ((1u << G) - 1u) << (lane & ~(G - 1));
     }
 }
 
-// Copy one placement row (n bytes at global byte offset `start` of `rows`)
-// into the group's 16-byte aligned buffer with 16-byte vector loads (streaming,
-// L1 no-allocate); the returned offset locates byte 0 of the row.
+// Copy one placement row (n bytes at global byte offset `start` of `rows`) into
+// the group's 16-byte aligned buffer with 16-byte streaming loads; returns the
+// offset of byte 0 of the row inside the buffer.
 template <int G>
 __device__ __forceinline__ int load_row(unsigned char *buf, const uint8_t *rows, long long start, int n,
-                                        long long rows_bytes, int gl) {
+                                        long long rows_bytes, int gl, bool live) {
     const long long a0 = start & ~15LL;
     const long long a1 = (start + n + 15) & ~15LL;
-    const int chunks = static_cast<int>((a1 - a0) >> 4);
+    const int chunks = live ? static_cast<int>((a1 - a0) >> 4) : 0;
     for (int c = gl; c < chunks; c += G) {
         const long long off = a0 + 16LL * c;
         uint4 v;
@@ -68,7 +80,7 @@ __device__ __forceinline__ int load_row(unsigned char *buf, const uint8_t *rows,
         }
         *reinterpret_cast<uint4 *>(buf + 16 * c) = v;
     }
-    return static_cast<int>(start - a0);
+    return live ? static_cast<int>(start - a0) : 0;
 }
 
 template <typename T>
@@ -87,8 +99,8 @@ struct RowResult {
     long long over_by;
 };
 
-// Stage the instance tables into shared memory (one elected thread issues
-// 1-D bulk async copies; every thread waits on the mbarrier's phase 0).
+// Stage the instance tables into shared memory (one elected thread issues 1-D
+// bulk async copies; every thread waits on the mbarrier's phase 0).
 __device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &a, uint64_t *bar) {
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -106,52 +118,63 @@ __device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &
     mbar_wait_parity(bar, 0);
 }
 
-// Evaluate the placement in `dev` (one device index per op) with the G lanes of
-// this group.  Every lane returns the same result.
-template <int G, bool TRACE>
-__device__ __forceinline__ RowResult eval_row(const EvalArgs &a, const unsigned char *tb, unsigned char *st,
-                                              const unsigned char *dev, int gl, unsigned gmask) {
+// Evaluate the placement `dev` of this group.  Called by all 32 lanes of the
+// warp together (lockstep); `live` = this group holds a real row.  Every lane
+// of a group returns the group's result.
+template <int G, bool TRACE, bool COLO>
+__device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsigned char *tb, unsigned char *st,
+                                                   unsigned char *dev, int gl, bool live) {
+    const int lane = threadIdx.x & 31;
+    const unsigned gbits = group_bits<G>(lane);
+    const unsigned below = gbits & ((1u << lane) - 1u);
     const int n_ops = a.n_ops;
     const int K = a.K;
-    const uint32_t DUMMY = static_cast<uint32_t>(3 * K);  // clock slot that always reads 0.0
+    const uint32_t RZ = static_cast<uint32_t>(3 * K);  // clock slot that always reads 0.0
+    const uint32_t WS = RZ + 1;                       // write sink for "no resource"
     const int rcap = a.rcap;
     RowResult res;
     res.ms = kInf;
+    res.status = MP_ROW_OK;
     res.over_dev = -1;
     res.over_by = 0;
 
-    // ---- 1. memory feasibility (solver.py:82-87) ----------------------------
-    unsigned long long *load = slot<unsigned long long>(st, a.so.load);
+    // ---- 1. memory feasibility (solver.py:82-87) ------------------------------
+    double *clk = slot<double>(st, a.so.clk);
+    unsigned long long *load = reinterpret_cast<unsigned long long *>(clk);
     for (int k = gl; k < K; k += G) load[k] = 0ULL;
-    __syncwarp(gmask);
+    __syncwarp();
     bool bad = false;
     for (int i = gl; i < n_ops; i += G) {
         const int d = dev[i];
         if (d >= K) {
             bad = true;
-        } else {
+        } else if (live) {
             atomicAdd(&load[d], static_cast<unsigned long long>(tab<long long>(tb, a.to.mem)[i]));
         }
     }
-    bad = __any_sync(gmask, bad);
-    __syncwarp(gmask);
-    if (bad) {
-        res.status = MP_ROW_BAD_DEVICE;
-        return res;
-    }
-    for (int k = 0; k < K; ++k) {
-        const long long l = static_cast<long long>(load[k]);
-        const long long c = tab<long long>(tb, a.to.cap)[k];
-        if (l > c) {
-            res.status = MP_ROW_MEMORY;
-            res.over_dev = k;
-            res.over_by = l - c;
-            return res;
+    __syncwarp();
+    bad = (__ballot_sync(kFull, bad) & gbits) != 0u;
+    if (live && !bad) {
+        for (int k = 0; k < K; ++k) {
+            const long long l = static_cast<long long>(load[k]);
+            const long long c = tab<long long>(tb, a.to.cap)[k];
+            if (l > c) {
+                res.status = MP_ROW_MEMORY;
+                res.over_dev = k;
+                res.over_by = l - c;
+                break;
+            }
         }
     }
+    if (bad) {
+        res.status = MP_ROW_BAD_DEVICE;
+        for (int i = gl; i < n_ops; i += G) dev[i] = 0;  // keep the lockstep passes in bounds
+    }
+    const bool alive = live && res.status == MP_ROW_OK;
+    __syncwarp();
 
+    // ---- 2+3. durations folded into the rank pass (solver.py:89-107) ------------
     double *rank = slot<double>(st, a.so.rank);
-    // ---- 2+3. durations folded into the rank pass (solver.py:89-107) -----------
     for (int lv = 0; lv < a.n_levels; ++lv) {
         const int b = static_cast<int>(tab<uint32_t>(tb, a.to.lvl_beg)[lv]);
         const int e = static_cast<int>(tab<uint32_t>(tb, a.to.lvl_beg)[lv + 1]);
@@ -161,181 +184,229 @@ __device__ __forceinline__ RowResult eval_row(const EvalArgs &a, const unsigned 
             double best = 0.0;
             const int qe = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[i + 1]);
             for (int q = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[i]); q < qe; ++q) {
-                const int f = static_cast<int>(tab<uint32_t>(tb, a.to.out_flow)[q]);
-                const int j = static_cast<int>(tab<uint32_t>(tb, a.to.fdst)[f]);
+                const int j = static_cast<int>(tab<uint32_t>(tb, a.to.s_dst)[q]);
                 const int dj = dev[j];
                 // rank of the flow node = dur + rank[j]   (rank[j] >= +0.0)
-                const double fr = (dj == d) ? rank[j]
-                                            : (tab<double>(tb, a.to.payload)[f] / tab<double>(tb, a.to.bw)[d * K + dj] +
-                                               rank[j]);
+                double fr = rank[j];
+                if (dj != d) fr = tab<double>(tb, a.to.s_pay)[q] / tab<double>(tb, a.to.bw)[d * K + dj] + fr;
                 if (fr > best) best = fr;
             }
             rank[i] = tab<double>(tb, a.to.cost)[i * K + d] + best;
         }
-        __syncwarp(gmask);
+        __syncwarp();
     }
 
-    // ---- 4. dispatch (solver.py:109-145) ----------------------------------------
-    double *est = slot<double>(st, a.so.est);
-    double *clk = slot<double>(st, a.so.clk);
+    // ---- 4. dispatch state (solver.py:109-116) ---------------------------------
+    double *m_est = slot<double>(st, a.so.m_est);
+    uint32_t *m_tie = slot<uint32_t>(st, a.so.m_tie);
+    uint16_t *m_np = slot<uint16_t>(st, a.so.m_np);
     double *r_est = slot<double>(st, a.so.r_est);
     double *r_rank = slot<double>(st, a.so.r_rank);
+    double *r_dur = slot<double>(st, a.so.r_dur);
     uint32_t *r_meta = slot<uint32_t>(st, a.so.r_meta);
-    uint16_t *npred = slot<uint16_t>(st, a.so.npred);
-    for (int i = gl; i < n_ops; i += G) {
-        npred[i] = tab<uint16_t>(tb, a.to.indeg)[i];
-        est[i] = 0.0;
+    uint32_t *r_tie = slot<uint32_t>(st, a.so.r_tie);
+    for (int k = gl; k < a.n_multi; k += G) {
+        m_np[k] = static_cast<uint16_t>(tab<uint32_t>(tb, a.to.m_deg)[k]);
+        m_est[k] = 0.0;
+        m_tie[k] = tab<uint32_t>(tb, a.to.m_op)[k];
     }
-    for (int k = gl; k <= static_cast<int>(DUMMY); k += G) clk[k] = 0.0;
+    for (int k = gl; k <= static_cast<int>(WS); k += G) clk[k] = 0.0;
     int nready = a.n_src;
-    bool ovf = nready > rcap;
-    if (!ovf) {
+    bool ovf = alive && nready > rcap;
+    if (alive && !ovf) {
         for (int t = gl; t < nready; t += G) {
             const int i = static_cast<int>(tab<uint32_t>(tb, a.to.srcs)[t]);
+            const int d = dev[i];
             r_est[t] = 0.0;
             r_rank[t] = rank[i];
-            r_meta[t] = static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev[i]) << 20) | (DUMMY << 26);
+            r_dur[t] = tab<double>(tb, a.to.cost)[i * K + d];
+            r_meta[t] = static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26);
+            r_tie[t] = static_cast<uint32_t>(i);
         }
     }
-    __syncwarp(gmask);
+    __syncwarp();
 
-    const int n_nodes = n_ops + a.n_flows;
+    bool done = !alive || ovf;
     double ms = 0.0;
-    for (int step = 0; step < n_nodes && !ovf; ++step) {
+    while (__any_sync(kFull, !done)) {
         // -- local minimum over this lane's slice of the ready set ----------------
+        const int maxr = __reduce_max_sync(kFull, done ? 0 : nready);
         unsigned long long be = ~0ULL, br = 0ULL;
-        uint32_t bn = 0xffffffffu;
+        uint32_t bi = 0xffffffffu, bmeta = 0;
+        double bdur = 0.0;
         int bs = -1;
-        for (int s = gl; s < nready; s += G) {
-            const uint32_t m = r_meta[s];
-            unsigned long long e = dbits(r_est[s]);
-            const unsigned long long c1 = dbits(clk[(m >> 20) & 63u]);
-            const unsigned long long c2 = dbits(clk[m >> 26]);
-            e = e > c1 ? e : c1;
-            e = e > c2 ? e : c2;
-            const unsigned long long r = dbits(r_rank[s]);
-            const uint32_t n = m & MP_NODE_MASK;
-            if (key_less(e, r, n, be, br, bn)) {
-                be = e;
-                br = r;
-                bn = n;
-                bs = s;
+        for (int s0 = 0; s0 < maxr; s0 += G) {
+            const int s = s0 + gl;
+            if (!done && s < nready) {
+                const uint32_t m = r_meta[s];
+                const unsigned long long es = dbits(r_est[s]);
+                const unsigned long long c1 = dbits(clk[(m >> 20) & 63u]);
+                const unsigned long long c2 = dbits(clk[m >> 26]);
+                unsigned long long e = es > c1 ? es : c1;
+                e = e > c2 ? e : c2;
+                const unsigned long long r = dbits(r_rank[s]);
+                const uint32_t id = (COLO && e == es) ? r_tie[s] : (m & MP_NODE_MASK);
+                if (key_less(e, r, id, be, br, bi)) {
+                    be = e;
+                    br = r;
+                    bi = id;
+                    bmeta = m;
+                    bdur = r_dur[s];
+                    bs = s;
+                }
             }
         }
-        const uint32_t mine = bn;
-        // -- G-lane butterfly: every lane ends with the group minimum --------------
+        const uint32_t mine = bi;
+        // -- G-lane butterfly: every lane ends with its group's minimum -----------
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) {
-            const unsigned long long e2 = __shfl_xor_sync(gmask, be, o, G);
-            const unsigned long long r2 = __shfl_xor_sync(gmask, br, o, G);
-            const uint32_t n2 = __shfl_xor_sync(gmask, bn, o, G);
-            if (key_less(e2, r2, n2, be, br, bn)) {
+            const unsigned long long e2 = __shfl_xor_sync(kFull, be, o, G);
+            const unsigned long long r2 = __shfl_xor_sync(kFull, br, o, G);
+            const uint32_t i2 = __shfl_xor_sync(kFull, bi, o, G);
+            if (key_less(e2, r2, i2, be, br, bi)) {
                 be = e2;
                 br = r2;
-                bn = n2;
+                bi = i2;
             }
         }
-        // -- remove the winner (swap with the last entry) ----------------------------
+        // -- the owning lane broadcasts the winner's meta / duration --------------
+        const bool owner = !done && bs >= 0 && mine == bi;
+        const unsigned own = __ballot_sync(kFull, owner) & gbits;
+        const int src_lane = own ? (__ffs(own) - 1) : lane;
+        const uint32_t wmeta = __shfl_sync(kFull, bmeta, src_lane);
+        const double wdur = __shfl_sync(kFull, bdur, src_lane);
         const int last = nready - 1;
-        if (mine == bn && bs != last) {
+        if (owner && bs != last) {  // unordered removal: move the last entry into the hole
             r_est[bs] = r_est[last];
             r_rank[bs] = r_rank[last];
+            r_dur[bs] = r_dur[last];
             r_meta[bs] = r_meta[last];
+            r_tie[bs] = r_tie[last];
         }
-        nready = last;
-        __syncwarp(gmask);
+        __syncwarp();
+        if (!done) nready = last;
 
+        // -- commit (solver.py:130-138): start = e, end = e + dur ----------------
         const double E = bitsd(be);
-        const int node = static_cast<int>(bn);
-        if (node < n_ops) {
-            // -- commit an op (solver.py:130-131,137-138) ----------------------------
-            const int d = dev[node];
-            const double end = E + tab<double>(tb, a.to.cost)[node * K + d];
-            if (end > ms) ms = end;
-            if (gl == 0) {
-                clk[d] = end;
-                if constexpr (TRACE) {
-                    a.starts[node] = E;
-                    a.ends[node] = end;
-                }
-            }
-            // its out-flows become ready with est = end (solver.py:140-145)
-            const int ob = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node]);
-            const int cnt = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node + 1]) - ob;
-            if (nready + cnt > rcap) {
-                ovf = true;
-            } else {
-                for (int t = gl; t < cnt; t += G) {
-                    const int f = static_cast<int>(tab<uint32_t>(tb, a.to.out_flow)[ob + t]);
-                    const int j = static_cast<int>(tab<uint32_t>(tb, a.to.fdst)[f]);
-                    const int dj = dev[j];
-                    double r;
-                    uint32_t m = static_cast<uint32_t>(n_ops + f);
-                    if (dj == d) {
-                        r = rank[j];
-                        m |= (DUMMY << 20) | (DUMMY << 26);
-                    } else {
-                        r = tab<double>(tb, a.to.payload)[f] / tab<double>(tb, a.to.bw)[d * K + dj] + rank[j];
-                        m |= (static_cast<uint32_t>(K + d) << 20) | (static_cast<uint32_t>(2 * K + dj) << 26);
-                    }
-                    r_est[nready + t] = end;
-                    r_rank[nready + t] = r;
-                    r_meta[nready + t] = m;
-                }
-                nready += cnt;
-            }
-        } else {
-            // -- commit a flow (solver.py:130-136) --------------------------------------
-            const int f = node - n_ops;
-            const int j = static_cast<int>(tab<uint32_t>(tb, a.to.fdst)[f]);
-            const int ka = dev[tab<uint32_t>(tb, a.to.fsrc)[f]];
-            const int kb = dev[j];
-            double end = E;
-            if (ka != kb) {
-                end = E + tab<double>(tb, a.to.payload)[f] / tab<double>(tb, a.to.bw)[ka * K + kb];
-                if (gl == 0) {
-                    clk[K + ka] = end;
-                    clk[2 * K + kb] = end;
-                }
-            }
+        const double end = E + wdur;
+        const int node = static_cast<int>(wmeta & MP_NODE_MASK);
+        const uint32_t r1 = (wmeta >> 20) & 63u, r2 = wmeta >> 26;
+        const bool isop = node < n_ops;
+        if (!done && gl == 0) {
+            clk[r1 == RZ ? WS : r1] = end;
+            clk[r2 == RZ ? WS : r2] = end;
             if constexpr (TRACE) {
-                if (gl == 0) {
-                    a.starts[node] = E;
-                    a.ends[node] = end;
-                }
-            }
-            // consumer bookkeeping (solver.py:140-145) by the group leader
-            int now_ready = 0;
-            if (gl == 0) {
-                const int np = static_cast<int>(npred[j]) - 1;
-                npred[j] = static_cast<uint16_t>(np);
-                double ej = est[j];
-                if (ej < end) {
-                    ej = end;
-                    est[j] = end;
-                }
-                if (np == 0) {
-                    now_ready = 1;
-                    if (nready < rcap) {
-                        r_est[nready] = ej;
-                        r_rank[nready] = rank[j];
-                        r_meta[nready] = static_cast<uint32_t>(j) | (static_cast<uint32_t>(kb) << 20) | (DUMMY << 26);
-                    }
-                }
-            }
-            now_ready = __shfl_sync(gmask, now_ready, 0, G);
-            if (now_ready) {
-                if (nready + 1 > rcap) ovf = true;
-                else nready += 1;
+                a.starts[node] = E;
+                a.ends[node] = end;
             }
         }
-        __syncwarp(gmask);
+        if (!done && isop && end > ms) ms = end;
+
+        // -- successors (solver.py:140-145) ---------------------------------------
+        // op    -> its out-flows (crossing ones enter the ready set; co-located ones
+        //          update their consumer directly in colo mode)
+        // flow  -> its destination op (npred-- / est max / maybe ready)
+        const int d = isop ? static_cast<int>(r1) : 0;
+        const int ob = (!done && isop) ? static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node]) : 0;
+        const int cnt = done ? 0 : (isop ? static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node + 1]) - ob : 1);
+        const int maxc = __reduce_max_sync(kFull, cnt);
+        for (int t0 = 0; t0 < maxc; t0 += G) {
+            const int t = t0 + gl;
+            bool ins = false;
+            double ne = 0.0, nr = 0.0, nd = 0.0;
+            uint32_t nm = 0, nt = 0;
+            if (t < cnt) {
+                int j;           // the op that may become ready
+                uint32_t pid;    // node id of the pred flow updating it
+                bool via_colo = false;
+                bool op_update = true;
+                if (isop) {
+                    const int q = ob + t;
+                    j = static_cast<int>(tab<uint32_t>(tb, a.to.s_dst)[q]);
+                    const int dj = dev[j];
+                    pid = static_cast<uint32_t>(n_ops) + tab<uint32_t>(tb, a.to.s_fid)[q];
+                    if (COLO && dj == d) {
+                        via_colo = true;  // zero-duration flow: start = end = producer's end
+                        if constexpr (TRACE) {
+                            a.starts[pid] = end;
+                            a.ends[pid] = end;
+                        }
+                    } else {
+                        op_update = false;
+                        double dur = 0.0;
+                        uint32_t m = pid;
+                        if (dj != d) {
+                            dur = tab<double>(tb, a.to.s_pay)[q] / tab<double>(tb, a.to.bw)[d * K + dj];
+                            m |= (static_cast<uint32_t>(K + d) << 20) | (static_cast<uint32_t>(2 * K + dj) << 26);
+                        } else {
+                            m |= (RZ << 20) | (RZ << 26);
+                        }
+                        ins = true;
+                        ne = end;
+                        nr = dur + rank[j];
+                        nd = dur;
+                        nm = m;
+                        nt = pid;
+                    }
+                } else {
+                    j = static_cast<int>(tab<uint32_t>(tb, a.to.fdst)[node - n_ops]);
+                    pid = static_cast<uint32_t>(node);
+                }
+                if (op_update) {
+                    const uint32_t k = tab<uint32_t>(tb, a.to.mi)[j];
+                    bool ready = true;
+                    double ej = end;
+                    uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+                    if (k != MP_NONE) {
+                        const int np = static_cast<int>(m_np[k]) - 1;
+                        m_np[k] = static_cast<uint16_t>(np);
+                        const double cur = m_est[k];
+                        uint32_t ct = m_tie[k];
+                        if (end > cur) {
+                            m_est[k] = end;
+                            ct = tj;
+                        } else {
+                            ej = cur;
+                            if (via_colo && end == cur && pid > ct) ct = pid;
+                        }
+                        m_tie[k] = ct;
+                        tj = ct;
+                        ready = np == 0;
+                    }
+                    if (ready) {
+                        const int dj = dev[j];
+                        ins = true;
+                        ne = ej;
+                        nr = rank[j];
+                        nd = tab<double>(tb, a.to.cost)[j * K + dj];
+                        nm = static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26);
+                        nt = tj;
+                    }
+                }
+            }
+            const unsigned bal = __ballot_sync(kFull, ins);
+            const int pos = nready + __popc(bal & below);
+            if (ins && pos < rcap) {
+                r_est[pos] = ne;
+                r_rank[pos] = nr;
+                r_dur[pos] = nd;
+                r_meta[pos] = nm;
+                r_tie[pos] = nt;
+            }
+            nready += __popc(bal & gbits);
+        }
+        if (!done && nready > rcap) {
+            ovf = true;
+            done = true;
+        }
+        if (!done && nready == 0) done = true;  // every node committed
+        __syncwarp();
     }
+    if (!alive) return res;
     if (ovf) {
         res.status = MP_ROW_OVERFLOW;
         return res;
     }
-    res.status = MP_ROW_OK;
     res.ms = ms;
     return res;
 }
@@ -363,62 +434,71 @@ __device__ __forceinline__ void cta_keep_best(const EvalArgs &a, double best_ms,
     }
 }
 
-}  // namespace
-
-// ---- K3/K4: batch evaluation with fused keep-best ---------------------------------
-template <int G, int SRC, bool ONCHIP, bool TRACE>
-__global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 4];
-    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 4];
-
-    const int lane = threadIdx.x & 31;
-    const int gl = lane & (G - 1);
-    const int grp = threadIdx.x / G;
-    const unsigned gmask = group_mask<G>(lane);
-
-    const unsigned char *tb;
-    unsigned char *st;
+template <bool ONCHIP>
+__device__ __forceinline__ void group_bases(unsigned char *sm, const EvalArgs &a, int grp, uint64_t *bar,
+                                            const unsigned char *&tb, unsigned char *&st) {
     if constexpr (ONCHIP) {
-        stage_tables(sm, a, &s_bar);
+        stage_tables(sm, a, bar);
         tb = sm;
         st = sm + a.to.bytes + static_cast<size_t>(grp) * a.so.bytes;
     } else {
         tb = a.blob;
         st = a.gstate + (static_cast<size_t>(blockIdx.x) * a.groups_per_cta + grp) * a.so.bytes;
     }
+}
+
+}  // namespace
+
+// ---- K3/K4: batch evaluation with fused keep-best ---------------------------------
+template <int G, int SRC, bool ONCHIP, bool TRACE, bool COLO>
+__global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 4];
+    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 4];
+    constexpr int GPW = 32 / G;  // groups per warp
+
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const int grp = threadIdx.x / G;
+    const unsigned char *tb;
+    unsigned char *st;
+    group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
     unsigned char *devbuf = st + a.so.dev;
+    for (int i = gl; i < a.n_ops + 16; i += G) devbuf[i] = 0;
     double best_ms = kInf;
     long long best_row = LLONG_MAX;
     const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
 
     for (;;) {
-        unsigned long long p = 0;
-        if (gl == 0) p = atomicAdd(a.next, 1ULL);
-        p = __shfl_sync(gmask, p, 0, G);
-        if (p >= static_cast<unsigned long long>(n_rows)) break;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next, static_cast<unsigned long long>(GPW));
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= static_cast<unsigned long long>(n_rows)) break;
+        const unsigned long long p = base + static_cast<unsigned long long>(lane / G);
+        const bool live = p < static_cast<unsigned long long>(n_rows);
 
-        long long grow;  // global row / enumeration index
-        const unsigned char *dev;
+        long long grow = 0;  // global row / enumeration index
+        unsigned char *dev;
         if constexpr (SRC == SRC_LOAD) {
-            const long long lrow = a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p);
+            const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
             grow = a.row_base + lrow;
             const int off = load_row<G>(devbuf, a.rows, lrow * static_cast<long long>(a.n_ops), a.n_ops,
-                                        a.rows_bytes, gl);
+                                        a.rows_bytes, gl, live);
             dev = devbuf + off;
         } else {
             const unsigned long long x = a.enum_first + p;
             grow = static_cast<long long>(x);
-            for (int t = gl; t < a.n_ops; t += G) {
-                devbuf[a.enum_order[t]] =
-                    static_cast<unsigned char>((x / a.enum_pow[t]) % static_cast<unsigned long long>(a.K));
+            if (live) {
+                for (int t = gl; t < a.n_ops; t += G)
+                    devbuf[a.enum_order[t]] =
+                        static_cast<unsigned char>((x / a.enum_pow[t]) % static_cast<unsigned long long>(a.K));
             }
             dev = devbuf;
         }
-        __syncwarp(gmask);
-        const RowResult r = eval_row<G, TRACE>(a, tb, st, dev, gl, gmask);
-        if (gl == 0) {
+        __syncwarp();
+        const RowResult r = eval_lockstep<G, TRACE, COLO>(a, tb, st, dev, gl, live);
+        if (live && gl == 0) {
             const long long o = grow - a.out_base;
             if (r.status == MP_ROW_OVERFLOW) {
                 const unsigned int k = atomicAdd(a.ovf_count, 1u);
@@ -431,11 +511,12 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __gri
                 if (a.overflow) a.overflow[o] = r.over_by;
             }
         }
-        if (r.status == MP_ROW_OK && r.ms < kInf && (r.ms < best_ms || (r.ms == best_ms && grow < best_row))) {
+        if (live && r.status == MP_ROW_OK && r.ms < kInf &&
+            (r.ms < best_ms || (r.ms == best_ms && grow < best_row))) {
             best_ms = r.ms;
             best_row = grow;
         }
-        __syncwarp(gmask);
+        __syncwarp();
     }
     if (a.want_argmin) cta_keep_best<G>(a, best_ms, best_row, gl, grp, s_best_ms, s_best_row);
 }
@@ -455,59 +536,59 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 // h = mix64(rng_seed ^ mix64(c * PHI + t)).  Accept iff the makespan does not
 // increase.  Proposals depend only on (rng_seed, c, t): results are identical
 // for any G, grid or GPU count.
-template <int G, bool ONCHIP>
+template <int G, bool ONCHIP, bool COLO>
 __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                      const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
+    constexpr int GPW = 32 / G;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const int grp = threadIdx.x / G;
-    const unsigned gmask = group_mask<G>(lane);
     const unsigned char *tb;
     unsigned char *st;
-    if constexpr (ONCHIP) {
-        stage_tables(sm, a, &s_bar);
-        tb = sm;
-        st = sm + a.to.bytes + static_cast<size_t>(grp) * a.so.bytes;
-    } else {
-        tb = a.blob;
-        st = a.gstate + (static_cast<size_t>(blockIdx.x) * a.groups_per_cta + grp) * a.so.bytes;
-    }
+    group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
     unsigned char *dev = st + a.so.dev;
+    for (int i = gl; i < a.n_ops + 16; i += G) dev[i] = 0;
     const int n = a.n_ops, K = a.K;
     for (;;) {
-        unsigned long long c = 0;
-        if (gl == 0) c = atomicAdd(a.next, 1ULL);
-        c = __shfl_sync(gmask, c, 0, G);
-        if (c >= static_cast<unsigned long long>(ls.n_chains)) break;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next, static_cast<unsigned long long>(GPW));
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= static_cast<unsigned long long>(ls.n_chains)) break;
+        const unsigned long long c = base + static_cast<unsigned long long>(lane / G);
+        const bool live = c < static_cast<unsigned long long>(ls.n_chains);
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
-        const uint8_t *seed = ls.seed_rows + (gc % static_cast<unsigned long long>(ls.n_seed)) * n;
-        for (int i = gl; i < n; i += G) dev[i] = seed[i];
-        __syncwarp(gmask);
-        RowResult cur = eval_row<G, false>(a, tb, st, dev, gl, gmask);
+        if (live) {
+            const uint8_t *seed = ls.seed_rows + (gc % static_cast<unsigned long long>(ls.n_seed)) * n;
+            for (int i = gl; i < n; i += G) dev[i] = seed[i];
+        }
+        __syncwarp();
+        RowResult cur = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live);
         double cur_ms = cur.status == MP_ROW_OK ? cur.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
             const int i = static_cast<int>((h & 0xffffffffULL) % static_cast<unsigned long long>(n));
             const int old = dev[i];
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
-            __syncwarp(gmask);
-            if (gl == 0) dev[i] = static_cast<unsigned char>(nd);
-            __syncwarp(gmask);
-            const RowResult r = eval_row<G, false>(a, tb, st, dev, gl, gmask);
+            __syncwarp();
+            if (live && gl == 0) dev[i] = static_cast<unsigned char>(nd);
+            __syncwarp();
+            const RowResult r = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live);
             const double ms = r.status == MP_ROW_OK ? r.ms : kInf;
-            __syncwarp(gmask);
+            __syncwarp();
             if (ms <= cur_ms) {
                 cur_ms = ms;
-            } else if (gl == 0) {
+            } else if (live && gl == 0) {
                 dev[i] = static_cast<unsigned char>(old);
             }
-            __syncwarp(gmask);
+            __syncwarp();
         }
-        for (int i = gl; i < n; i += G) ls.chain_rows[c * n + i] = dev[i];
-        if (gl == 0) ls.chain_ms[c] = cur_ms;
-        __syncwarp(gmask);
+        if (live) {
+            for (int i = gl; i < n; i += G) ls.chain_rows[c * n + i] = dev[i];
+            if (gl == 0) ls.chain_ms[c] = cur_ms;
+        }
+        __syncwarp();
     }
 }
 
@@ -575,7 +656,7 @@ __global__ void mp_ls_pick_kernel(const double *chain_ms, long long n, double *o
     }
     if (threadIdx.x == 0) {
         *out_ms = sm_ms[0];
-        *out_c = sm_c[0];
+        *out_c = sm_c[0] == LLONG_MAX ? 0 : sm_c[0];
     }
 }
 
@@ -584,65 +665,73 @@ namespace {
 typedef void (*EvalFn)(const EvalArgs);
 typedef void (*LsFn)(const EvalArgs, const LsArgs);
 
-template <int G>
-EvalFn pick(int src, bool onchip, bool trace) {
-    if (src == SRC_LOAD) {
-        if (onchip) return trace ? mp_eval_kernel<G, SRC_LOAD, true, true> : mp_eval_kernel<G, SRC_LOAD, true, false>;
-        return trace ? mp_eval_kernel<G, SRC_LOAD, false, true> : mp_eval_kernel<G, SRC_LOAD, false, false>;
-    }
-    if (onchip) return mp_eval_kernel<G, SRC_ENUM, true, false>;
-    return mp_eval_kernel<G, SRC_ENUM, false, false>;
+template <int G, bool COLO>
+EvalFn pick_g(int src, bool onchip, bool trace) {
+    if (trace) return mp_eval_kernel<G, SRC_LOAD, false, true, COLO>;
+    if (src == SRC_LOAD)
+        return onchip ? mp_eval_kernel<G, SRC_LOAD, true, false, COLO> : mp_eval_kernel<G, SRC_LOAD, false, false, COLO>;
+    return onchip ? mp_eval_kernel<G, SRC_ENUM, true, false, COLO> : mp_eval_kernel<G, SRC_ENUM, false, false, COLO>;
 }
 
-EvalFn pick_any(int G, int src, bool onchip, bool trace) {
+template <bool COLO>
+EvalFn pick_c(int G, int src, bool onchip, bool trace) {
     switch (G) {
-        case 4: return pick<4>(src, onchip, trace);
-        case 8: return pick<8>(src, onchip, trace);
-        case 16: return pick<16>(src, onchip, trace);
-        default: return pick<32>(src, onchip, trace);
+        case 2: return pick_g<2, COLO>(src, onchip, trace);
+        case 4: return pick_g<4, COLO>(src, onchip, trace);
+        case 8: return pick_g<8, COLO>(src, onchip, trace);
+        case 16: return pick_g<16, COLO>(src, onchip, trace);
+        default: return pick_g<32, COLO>(src, onchip, trace);
     }
 }
 
-LsFn pick_ls(int G, bool onchip) {
+EvalFn pick_any(int G, int src, bool onchip, bool trace, bool colo) {
+    return colo ? pick_c<true>(G, src, onchip, trace) : pick_c<false>(G, src, onchip, trace);
+}
+
+template <bool COLO>
+LsFn pick_ls_c(int G, bool onchip) {
     switch (G) {
-        case 4: return onchip ? mp_ls_kernel<4, true> : mp_ls_kernel<4, false>;
-        case 8: return onchip ? mp_ls_kernel<8, true> : mp_ls_kernel<8, false>;
-        case 16: return onchip ? mp_ls_kernel<16, true> : mp_ls_kernel<16, false>;
-        default: return onchip ? mp_ls_kernel<32, true> : mp_ls_kernel<32, false>;
+        case 2: return onchip ? mp_ls_kernel<2, true, COLO> : mp_ls_kernel<2, false, COLO>;
+        case 4: return onchip ? mp_ls_kernel<4, true, COLO> : mp_ls_kernel<4, false, COLO>;
+        case 8: return onchip ? mp_ls_kernel<8, true, COLO> : mp_ls_kernel<8, false, COLO>;
+        case 16: return onchip ? mp_ls_kernel<16, true, COLO> : mp_ls_kernel<16, false, COLO>;
+        default: return onchip ? mp_ls_kernel<32, true, COLO> : mp_ls_kernel<32, false, COLO>;
     }
 }
+
+LsFn pick_ls(int G, bool onchip, bool colo) { return colo ? pick_ls_c<true>(G, onchip) : pick_ls_c<false>(G, onchip); }
 }  // namespace
 
 cudaError_t mp_eval_set_smem_limits() {
     static bool done = false;
     if (done) return cudaSuccess;
-    const int Gs[4] = {4, 8, 16, 32};
-    for (int gi = 0; gi < 4; ++gi) {
-        for (int src = 0; src < 2; ++src) {
-            for (int tr = 0; tr < 2; ++tr) {
-                EvalFn f = pick_any(Gs[gi], src, true, tr != 0);
+    const int Gs[5] = {2, 4, 8, 16, 32};
+    for (int gi = 0; gi < 5; ++gi) {
+        for (int colo = 0; colo < 2; ++colo) {
+            for (int src = 0; src < 2; ++src) {
+                EvalFn f = pick_any(Gs[gi], src, true, false, colo != 0);
                 cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
                 if (e != cudaSuccess) return e;
             }
+            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(pick_ls(Gs[gi], true, colo != 0)),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+            if (e != cudaSuccess) return e;
         }
-        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(pick_ls(Gs[gi], true)),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
-        if (e != cudaSuccess) return e;
     }
     done = true;
     return cudaSuccess;
 }
 
 cudaError_t mp_launch_eval(const LaunchShape &ls, int src_mode, bool trace, const EvalArgs &a, cudaStream_t s) {
-    EvalFn f = pick_any(ls.G, src_mode, ls.onchip, trace);
-    f<<<ls.ctas, ls.threads, ls.onchip ? ls.smem : 0, s>>>(a);
+    EvalFn f = pick_any(ls.G, src_mode, ls.onchip && !trace, trace, a.colo != 0);
+    f<<<ls.ctas, ls.threads, (ls.onchip && !trace) ? ls.smem : 0, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
 }
 
 cudaError_t mp_launch_ls(const LaunchShape &shape, const EvalArgs &a, const LsArgs &ls, cudaStream_t s) {
-    LsFn f = pick_ls(shape.G, shape.onchip);
+    LsFn f = pick_ls(shape.G, shape.onchip, a.colo != 0);
     f<<<shape.ctas, shape.threads, shape.onchip ? shape.smem : 0, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();

@@ -25,6 +25,12 @@ namespace {
 
 constexpr int kBuildThreads = 1024;
 
+inline double __longlong_as_double_host(unsigned long long b) {
+    double d;
+    memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
 inline uint32_t align16(uint64_t x) { return static_cast<uint32_t>((x + 15) & ~15ULL); }
 
 int set_err(mp_error *err, int code, int64_t a, int64_t b, const char *fmt, ...) {
@@ -50,6 +56,10 @@ int set_err(mp_error *err, int code, int64_t a, int64_t b, const char *fmt, ...)
 
 // ---- build kernels ------------------------------------------------------------
 struct BuildErr {
+    unsigned long long min_cost_bits;   // smallest op cost (bits of a non-negative double)
+    unsigned long long max_cost_bits;   // largest op cost
+    unsigned long long max_bw_bits;     // largest off-diagonal bandwidth
+    long long min_payload;
     unsigned long long missing;   // first (op*K + dev) with NaN cost
     unsigned long long bad_flow;  // first flow with an endpoint out of range
     unsigned int max_indeg;
@@ -61,49 +71,86 @@ struct BuildErr {
 __global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cost, const long long *mem,
                                 const int *fsrc, const int *fdst, const long long *payload,
                                 const long long *cap, const double *bw, unsigned char *blob, TabOff to,
-                                unsigned int *outdeg, unsigned int *indeg32, BuildErr *be) {
+                                unsigned int *outdeg, unsigned int *indeg32, double *pay_d, BuildErr *be) {
     const int stride = gridDim.x * blockDim.x;
     const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
     double *bcost = reinterpret_cast<double *>(blob + to.cost);
     long long *bmem = reinterpret_cast<long long *>(blob + to.mem);
-    double *bpay = reinterpret_cast<double *>(blob + to.payload);
     double *bbw = reinterpret_cast<double *>(blob + to.bw);
     long long *bcap = reinterpret_cast<long long *>(blob + to.cap);
-    uint32_t *bsrc = reinterpret_cast<uint32_t *>(blob + to.fsrc);
     uint32_t *bdst = reinterpret_cast<uint32_t *>(blob + to.fdst);
     const long long nc = static_cast<long long>(n_ops) * K;
     for (long long x = t0; x < nc; x += stride) {
         const double c = cost[x];
-        if (isnan(c)) atomicMin(&be->missing, static_cast<unsigned long long>(x));
+        if (isnan(c)) {
+            atomicMin(&be->missing, static_cast<unsigned long long>(x));
+        } else {
+            // costs are >= 0 (OpNode validation); -0.0 counts as zero
+            const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(c == 0.0 ? 0.0 : c));
+            atomicMin(&be->min_cost_bits, b);
+            atomicMax(&be->max_cost_bits, b);
+        }
         bcost[x] = c;
     }
     for (int i = t0; i < n_ops; i += stride) bmem[i] = mem[i];
-    for (int k = t0; k < K * K; k += stride) bbw[k] = bw[k];
+    for (int k = t0; k < K * K; k += stride) {
+        bbw[k] = bw[k];
+        if (k / K != k % K) atomicMax(&be->max_bw_bits, static_cast<unsigned long long>(__double_as_longlong(bw[k])));
+    }
     for (int k = t0; k < K; k += stride) bcap[k] = cap[k];
     for (int f = t0; f < n_flows; f += stride) {
         const int s = fsrc[f], d = fdst[f];
         // Python int -> float conversion is correctly rounded, as is this cast.
-        bpay[f] = static_cast<double>(payload[f]);
+        pay_d[f] = static_cast<double>(payload[f]);
+        atomicMin(&be->min_payload, payload[f]);
         if (s < 0 || s >= n_ops || d < 0 || d >= n_ops || s == d) {
             atomicMin(&be->bad_flow, static_cast<unsigned long long>(f));
-            bsrc[f] = 0;
             bdst[f] = 0;
             continue;
         }
-        bsrc[f] = static_cast<uint32_t>(s);
         bdst[f] = static_cast<uint32_t>(d);
         atomicAdd(&outdeg[s], 1u);
         atomicAdd(&indeg32[d], 1u);
     }
 }
 
-__global__ void k_indeg16(int n_ops, const unsigned int *indeg32, unsigned char *blob, TabOff to,
-                          unsigned char *is_src, BuildErr *be) {
-    uint16_t *b = reinterpret_cast<uint16_t *>(blob + to.indeg);
+// flow slots in source order: s_fid = sorted flow index, s_dst / s_pay gathered
+__global__ void k_slots(int n_flows, const unsigned int *sorted_f, const int *fdst, const double *pay_d,
+                        unsigned char *blob, TabOff to) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_flows; q += gridDim.x * blockDim.x) {
+        const unsigned int f = sorted_f[q];
+        reinterpret_cast<uint32_t *>(blob + to.s_fid)[q] = f;
+        reinterpret_cast<uint32_t *>(blob + to.s_dst)[q] = static_cast<uint32_t>(fdst[f]);
+        reinterpret_cast<double *>(blob + to.s_pay)[q] = pay_d[f];
+    }
+}
+
+// multi-input map: mi[j] = rank of j among ops with in-degree >= 2
+__global__ void k_multi(int n_ops, const unsigned int *indeg32, const unsigned int *mscan, unsigned char *blob,
+                        TabOff to) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_ops; j += gridDim.x * blockDim.x) {
+        const unsigned int d = indeg32[j];
+        uint32_t *mi = reinterpret_cast<uint32_t *>(blob + to.mi);
+        if (d >= 2) {
+            const unsigned int k = mscan[j];
+            mi[j] = k;
+            reinterpret_cast<uint32_t *>(blob + to.m_op)[k] = static_cast<uint32_t>(j);
+            reinterpret_cast<uint32_t *>(blob + to.m_deg)[k] = d;
+        } else {
+            mi[j] = MP_NONE;
+        }
+    }
+}
+
+__global__ void k_flag_multi(int n_ops, const unsigned int *indeg32, unsigned int *flag) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_ops; j += gridDim.x * blockDim.x)
+        flag[j] = indeg32[j] >= 2 ? 1u : 0u;
+}
+
+__global__ void k_indeg_stats(int n_ops, const unsigned int *indeg32, unsigned char *is_src, BuildErr *be) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += gridDim.x * blockDim.x) {
         const unsigned int d = indeg32[i];
         atomicMax(&be->max_indeg, d);
-        b[i] = static_cast<uint16_t>(d > 65535u ? 65535u : d);
         is_src[i] = d == 0 ? 1 : 0;
     }
 }
@@ -119,7 +166,7 @@ __global__ void k_iota(int n, unsigned int *v) {
 // above a cycle.
 __global__ void __launch_bounds__(kBuildThreads) k_heights(int n_ops, const unsigned int *in_beg,
                                                            const unsigned int *in_flow,
-                                                           const uint32_t *fsrc, unsigned int *outcnt,
+                                                           const int *fsrc, unsigned int *outcnt,
                                                            unsigned int *height, unsigned int *fa,
                                                            unsigned int *fb, BuildErr *be) {
     __shared__ unsigned int s_next, s_cur;
@@ -145,7 +192,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_heights(int n_ops, const unsi
         for (unsigned int t = threadIdx.x; t < n; t += blockDim.x) {
             const unsigned int i = cur[t];
             for (unsigned int q = in_beg[i]; q < in_beg[i + 1]; ++q) {
-                const unsigned int u = fsrc[in_flow[q]];
+                const unsigned int u = static_cast<unsigned int>(fsrc[in_flow[q]]);
                 if (atomicSub(&outcnt[u], 1u) == 1u) {
                     height[u] = h + 1;
                     nxt[atomicAdd(&s_next, 1u)] = u;
@@ -181,8 +228,7 @@ __global__ void k_level_bounds(int n_ops, const unsigned int *sorted_h, unsigned
     }
 }
 
-// Evaluator variants that are on-chip need their slot offsets; both kinds use this.
-StOff make_stoff(int n_ops, int K, int rcap) {
+StOff make_stoff(int n_ops, int n_multi, int K, int rcap) {
     StOff s{};
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) {
@@ -191,13 +237,15 @@ StOff make_stoff(int n_ops, int K, int rcap) {
         return at;
     };
     s.rank = take(8ULL * n_ops);
-    s.est = take(8ULL * n_ops);
-    s.clk = take(8ULL * (3 * K + 1));
-    s.load = take(8ULL * K);
+    s.m_est = take(8ULL * n_multi);
+    s.clk = take(8ULL * (3 * K + 2));
     s.r_est = take(8ULL * rcap);
     s.r_rank = take(8ULL * rcap);
+    s.r_dur = take(8ULL * rcap);
     s.r_meta = take(4ULL * rcap);
-    s.npred = take(2ULL * n_ops);
+    s.r_tie = take(4ULL * rcap);
+    s.m_tie = take(4ULL * n_multi);
+    s.m_np = take(2ULL * n_multi);
     s.dev = take(static_cast<uint64_t>(n_ops) + 32);
     s.bytes = static_cast<uint32_t>(o);
     return s;
@@ -213,14 +261,16 @@ TabOff make_taboff(int n_ops, int n_flows, int K) {
     };
     t.cost = take(8ULL * n_ops * K);
     t.mem = take(8ULL * n_ops);
-    t.payload = take(8ULL * n_flows);
     t.bw = take(8ULL * K * K);
     t.cap = take(8ULL * K);
     t.out_beg = take(4ULL * (n_ops + 1));
-    t.out_flow = take(4ULL * n_flows);
-    t.fsrc = take(4ULL * n_flows);
+    t.s_dst = take(4ULL * n_flows);
+    t.s_fid = take(4ULL * n_flows);
+    t.s_pay = take(8ULL * n_flows);
     t.fdst = take(4ULL * n_flows);
-    t.indeg = take(2ULL * n_ops);
+    t.mi = take(4ULL * n_ops);
+    t.m_op = take(4ULL * n_ops);   // n_multi <= n_ops
+    t.m_deg = take(4ULL * n_ops);
     t.lvl_ops = take(4ULL * n_ops);
     t.lvl_beg = take(4ULL * (n_ops + 1));
     t.srcs = take(4ULL * n_ops);
@@ -250,9 +300,12 @@ struct DevBuf {
 struct mp_instance {
     int device = 0;
     int n_ops = 0, n_flows = 0, K = 0, n_nodes = 0;
-    int n_levels = 0, n_src = 0, n_sinks = 0;
+    int n_levels = 0, n_src = 0, n_sinks = 0, n_multi = 0;
     int ready_bound = 0;   // min-path-cover bound on any ready set
+    bool colo_ok = false;  // every op cost and crossing-flow duration > 0
+    bool colo = false;     // co-located flows skipped
     int sms = 0;
+    int rcap_target = 32;
     TabOff to{};
     unsigned char *blob = nullptr;
     // main (on-chip when possible) and off-chip variants
@@ -282,11 +335,11 @@ void choose_shapes(mp_instance *I, int G_req, int ctas_per_sm_req) {
     // Ready sets are antichains of the augmented DAG, so a vertex-disjoint path
     // cover bounds them: every non-sink op continues into one out-flow and every
     // non-source op is continued by one in-flow -> n_flows - n_ops + n_src + n_sinks
-    // paths.  Within 256 the bound is the on-chip capacity (no overflow possible);
-    // above it, 128 slots plus the off-chip re-run of overflowing rows.
-    int rcap = I->ready_bound <= 256 ? std::max(1, I->ready_bound) : 128;
-    StOff so = make_stoff(n_ops, K, rcap);
-    int G = G_req > 0 ? G_req : 8;
+    // paths.  On chip the capacity is min(bound, 32): rows whose ready set
+    // outgrows it are re-run by the off-chip variant with capacity = bound.
+    int rcap = std::max(1, std::min(I->ready_bound, I->rcap_target));
+    StOff so = make_stoff(n_ops, I->n_multi, K, rcap);
+    int G = G_req > 0 ? G_req : (I->ready_bound <= 16 ? 4 : 8);
     const int per_warp = 32 / G;
     const long long avail = static_cast<long long>(smem_cap) - I->to.bytes;
     long long groups_fit = avail > 0 ? avail / so.bytes : 0;
@@ -310,7 +363,7 @@ void choose_shapes(mp_instance *I, int G_req, int ctas_per_sm_req) {
         I->main.onchip = false;
     }
     // off-chip variant: one warp per placement, full ready capacity
-    StOff wso = make_stoff(n_ops, K, std::max(1, I->ready_bound));
+    StOff wso = make_stoff(n_ops, I->n_multi, K, std::max(1, I->ready_bound));
     LaunchShape w{};
     w.G = 32;
     w.threads = 256;
@@ -341,6 +394,8 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.K = I->K;
     a.n_levels = I->n_levels;
     a.n_src = I->n_src;
+    a.n_multi = I->n_multi;
+    a.colo = I->colo ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
     a.gstate = static_cast<unsigned char *>(wide ? I->wide_state.p : I->main_state.p);
@@ -439,15 +494,21 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     memcpy(host.data() + off_cap, prob->cap, b_cap);
     memcpy(host.data() + off_bw, prob->bw, b_bw);
 
-    // scratch: raw | outdeg | indeg32 | outcnt | height | fa | fb | iota | sorted keys/vals | is_src | cub tmp | err
+    // scratch: raw | outdeg | indeg32 | outcnt | height | fa | fb | iota | keys | in_beg | in_flow | sorted_f |
+    //          mflag | mscan | pay_d | is_src | nsel | err | cub tmp
     const size_t nA = static_cast<size_t>(n_ops) + 1, nF = static_cast<size_t>(std::max(n_flows, 1));
-    size_t s_outdeg = raw_bytes, s_indeg = align16(s_outdeg + 4 * nA), s_outcnt = align16(s_indeg + 4 * nA),
-           s_height = align16(s_outcnt + 4 * nA), s_fa = align16(s_height + 4 * nA), s_fb = align16(s_fa + 4 * nA),
-           s_iota = align16(s_fb + 4 * nA), s_keys = align16(s_iota + 4 * std::max(nA, nF)),
-           s_in_beg = align16(s_keys + 4 * std::max(nA, nF)), s_in_flow = align16(s_in_beg + 4 * nA),
-           s_issrc = align16(s_in_flow + 4 * nF), s_nsel = align16(s_issrc + nA), s_err = align16(s_nsel + 16),
-           s_tmp = align16(s_err + sizeof(BuildErr));
-    // cub temp size
+    size_t cur = raw_bytes;
+    auto carve = [&](size_t bytes) {
+        const size_t at = cur;
+        cur = align16(cur + bytes);
+        return at;
+    };
+    const size_t s_outdeg = carve(4 * nA), s_indeg = carve(4 * nA), s_outcnt = carve(4 * nA),
+                 s_height = carve(4 * nA), s_fa = carve(4 * nA), s_fb = carve(4 * nA),
+                 s_iota = carve(4 * std::max(nA, nF)), s_keys = carve(4 * std::max(nA, nF)), s_in_beg = carve(4 * nA),
+                 s_in_flow = carve(4 * nF), s_sorted_f = carve(4 * nF), s_mflag = carve(4 * nA),
+                 s_mscan = carve(4 * nA), s_pay = carve(8 * nF), s_issrc = carve(nA), s_nsel = carve(16),
+                 s_err = carve(sizeof(BuildErr)), s_tmp = cur;
     size_t tmp1 = 0, tmp2 = 0, tmp3 = 0, tmp4 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp1, (const unsigned int *)nullptr, (unsigned int *)nullptr,
                                     (const unsigned int *)nullptr, (unsigned int *)nullptr, static_cast<int>(nF));
@@ -467,6 +528,10 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     BuildErr *d_be = reinterpret_cast<BuildErr *>(S + s_err);
     {
         BuildErr init{};
+        init.min_cost_bits = ~0ULL;
+        init.max_cost_bits = 0;
+        init.max_bw_bits = 0;
+        init.min_payload = LLONG_MAX;
         init.missing = ~0ULL;
         init.bad_flow = ~0ULL;
         MP_CUDA_I(cudaMemcpyAsync(d_be, &init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
@@ -481,20 +546,25 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     unsigned int *keys = reinterpret_cast<unsigned int *>(S + s_keys);
     unsigned int *in_beg = reinterpret_cast<unsigned int *>(S + s_in_beg);
     unsigned int *in_flow = reinterpret_cast<unsigned int *>(S + s_in_flow);
+    unsigned int *sorted_f = reinterpret_cast<unsigned int *>(S + s_sorted_f);
+    unsigned int *mflag = reinterpret_cast<unsigned int *>(S + s_mflag);
+    unsigned int *mscan = reinterpret_cast<unsigned int *>(S + s_mscan);
+    double *pay_d = reinterpret_cast<double *>(S + s_pay);
     unsigned char *is_src = S + s_issrc;
     int *nsel = reinterpret_cast<int *>(S + s_nsel);
     void *tmp = S + s_tmp;
+    const int *raw_src = reinterpret_cast<const int *>(S + off_src);
+    const int *raw_dst = reinterpret_cast<const int *>(S + off_dst);
 
     const int gridN = std::max(1, std::min(1024, (std::max(n_ops * K, n_flows) + 255) / 256));
     k_copy_validate<<<gridN, 256, 0, I->stream>>>(
         n_ops, n_flows, K, reinterpret_cast<const double *>(S + off_cost),
-        reinterpret_cast<const long long *>(S + off_mem), reinterpret_cast<const int *>(S + off_src),
-        reinterpret_cast<const int *>(S + off_dst), reinterpret_cast<const long long *>(S + off_pay),
-        reinterpret_cast<const long long *>(S + off_cap), reinterpret_cast<const double *>(S + off_bw), I->blob,
-        I->to, outdeg, indeg32, d_be);
+        reinterpret_cast<const long long *>(S + off_mem), raw_src, raw_dst,
+        reinterpret_cast<const long long *>(S + off_pay), reinterpret_cast<const long long *>(S + off_cap),
+        reinterpret_cast<const double *>(S + off_bw), I->blob, I->to, outdeg, indeg32, pay_d, d_be);
     ++g_mp_launches;
     MP_CUDA_I(cudaGetLastError());
-    k_indeg16<<<gridN, 256, 0, I->stream>>>(n_ops, indeg32, I->blob, I->to, is_src, d_be);
+    k_indeg_stats<<<gridN, 256, 0, I->stream>>>(n_ops, indeg32, is_src, d_be);
     ++g_mp_launches;
     BuildErr be{};
     MP_CUDA_I(cudaMemcpyAsync(&be, d_be, sizeof(be), cudaMemcpyDeviceToHost, I->stream));
@@ -510,14 +580,11 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         return fail(set_err(err, MP_ERR_UNSUPPORTED, be.max_indeg, 65535, "op in-degree %u > 65535", be.max_indeg));
 
     uint32_t *b_out_beg = reinterpret_cast<uint32_t *>(I->blob + I->to.out_beg);
-    uint32_t *b_out_flow = reinterpret_cast<uint32_t *>(I->blob + I->to.out_flow);
-    const uint32_t *b_fsrc = reinterpret_cast<const uint32_t *>(I->blob + I->to.fsrc);
-    const uint32_t *b_fdst = reinterpret_cast<const uint32_t *>(I->blob + I->to.fdst);
     uint32_t *b_lvl_ops = reinterpret_cast<uint32_t *>(I->blob + I->to.lvl_ops);
     uint32_t *b_lvl_beg = reinterpret_cast<uint32_t *>(I->blob + I->to.lvl_beg);
     uint32_t *b_srcs = reinterpret_cast<uint32_t *>(I->blob + I->to.srcs);
 
-    // out-flow CSR: exclusive scan of out-degrees, stable sort of flows by source
+    // out-flow slots: exclusive scan of out-degrees, stable sort of flows by source
     size_t tb = tmpb;
     MP_CUDA_I(cub::DeviceScan::ExclusiveSum(tmp, tb, outdeg, b_out_beg, n_ops + 1, I->stream));
     tb = tmpb;
@@ -526,13 +593,27 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         k_iota<<<gridN, 256, 0, I->stream>>>(n_flows, iota);
         ++g_mp_launches;
         tb = tmpb;
-        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, b_fsrc, keys, iota, b_out_flow, n_flows, 0, 32, I->stream));
+        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, reinterpret_cast<const unsigned int *>(raw_src), keys, iota,
+                                                  sorted_f, n_flows, 0, 32, I->stream));
+        k_slots<<<gridN, 256, 0, I->stream>>>(n_flows, sorted_f, raw_dst, pay_d, I->blob, I->to);
+        ++g_mp_launches;
         tb = tmpb;
-        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, b_fdst, keys, iota, in_flow, n_flows, 0, 32, I->stream));
+        MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, reinterpret_cast<const unsigned int *>(raw_dst), keys, iota,
+                                                  in_flow, n_flows, 0, 32, I->stream));
     }
+    // multi-input map (est / npred / gate state only for ops with >= 2 in-flows)
+    k_flag_multi<<<gridN, 256, 0, I->stream>>>(n_ops, indeg32, mflag);
+    ++g_mp_launches;
+    MP_CUDA_I(cudaMemsetAsync(mflag + n_ops, 0, 4, I->stream));
+    tb = tmpb;
+    MP_CUDA_I(cub::DeviceScan::ExclusiveSum(tmp, tb, mflag, mscan, n_ops + 1, I->stream));
+    k_multi<<<gridN, 256, 0, I->stream>>>(n_ops, indeg32, mscan, I->blob, I->to);
+    ++g_mp_launches;
+    unsigned int h_multi = 0;
+    MP_CUDA_I(cudaMemcpyAsync(&h_multi, mscan + n_ops, 4, cudaMemcpyDeviceToHost, I->stream));
     // heights (rank-pass levels) + cycle check
     MP_CUDA_I(cudaMemcpyAsync(outcnt, outdeg, 4ULL * n_ops, cudaMemcpyDeviceToDevice, I->stream));
-    k_heights<<<1, kBuildThreads, 0, I->stream>>>(n_ops, in_beg, in_flow, b_fsrc, outcnt, height, fa, fb, d_be);
+    k_heights<<<1, kBuildThreads, 0, I->stream>>>(n_ops, in_beg, in_flow, raw_src, outcnt, height, fa, fb, d_be);
     ++g_mp_launches;
     MP_CUDA_I(cudaMemcpyAsync(&be, d_be, sizeof(be), cudaMemcpyDeviceToHost, I->stream));
     MP_CUDA_I(cudaStreamSynchronize(I->stream));
@@ -540,6 +621,7 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         return fail(set_err(err, MP_ERR_CYCLE, n_ops - static_cast<int64_t>(be.processed), 0,
                             "graph contains a cycle"));
     I->n_levels = static_cast<int>(be.n_levels);
+    I->n_multi = static_cast<int>(h_multi);
     // bucket ops by height (stable: ascending op index inside a level)
     k_iota<<<gridN, 256, 0, I->stream>>>(n_ops, iota);
     ++g_mp_launches;
@@ -556,6 +638,18 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     I->n_src = h_nsel;
     I->n_sinks = static_cast<int>(be.n_sinks);
     I->ready_bound = std::min(I->n_nodes, n_flows - n_ops + I->n_src + I->n_sinks);
+    // Skipping co-located flows is exact when every op cost and every crossing
+    // flow duration payload/bw is strictly positive and finite.
+    {
+        const double min_cost = __longlong_as_double_host(be.min_cost_bits);
+        const double max_cost = __longlong_as_double_host(be.max_cost_bits);
+        const double max_bw = __longlong_as_double_host(be.max_bw_bits);
+        bool ok = min_cost > 0.0 && std::isfinite(max_cost);
+        if (n_flows > 0) ok = ok && be.min_payload > 0 && std::isfinite(max_bw) && K > 1 &&
+                              (static_cast<double>(be.min_payload) / max_bw) > 0.0;
+        I->colo_ok = ok;
+        I->colo = ok;
+    }
 
     choose_shapes(I, 0, 0);
     *out = I;
@@ -592,16 +686,25 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->smem_bytes = I->main.onchip ? I->main.smem : 0;
     info->onchip = I->main.onchip ? 1 : 0;
     info->device = I->device;
+    info->n_multi = I->n_multi;
+    info->ready_bound = I->ready_bound;
+    info->colo = I->colo ? 1 : 0;
+    info->colo_ok = I->colo_ok ? 1 : 0;
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
     return MP_OK;
 }
 
-int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t ctas_per_sm) {
+int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t ctas_per_sm, int32_t ready_cap,
+                         uint32_t flags) {
     if (!I) return MP_ERR_INVALID;
-    if (group_lanes != 0 && group_lanes != 4 && group_lanes != 8 && group_lanes != 16 && group_lanes != 32)
+    if (group_lanes != 0 && group_lanes != 2 && group_lanes != 4 && group_lanes != 8 && group_lanes != 16 &&
+        group_lanes != 32)
         return MP_ERR_INVALID;
+    if (ready_cap < 0 || ctas_per_sm < 0) return MP_ERR_INVALID;
     std::lock_guard<std::mutex> lk(I->mu);
+    I->rcap_target = ready_cap > 0 ? ready_cap : 32;
+    I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     choose_shapes(I, group_lanes, ctas_per_sm);
     return MP_OK;
 }

@@ -1,0 +1,77 @@
+"""Time the evaluator kernel on device-resident placements for several launch
+shapes (lanes per placement G); optional single config for ncu.
+
+python scripts/prof_eval.py [--workload c2] [--rows 262144] [--G 4,8,16,32] [--iters 3]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2312_04025_b200 as mp  # noqa: E402
+from paper_2312_04025_b200 import _native as N  # noqa: E402
+from paper_2312_04025_b200 import workloads  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--rows", type=int, default=1 << 18)
+    ap.add_argument("--G", default="4,8,16,32")
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    args = ap.parse_args()
+    w = {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c2k8": lambda: workloads.c2(8),
+         "c3": workloads.c3, "c4": workloads.c4}[args.workload]()
+    coarse = mp.gcof(w.raw, w.rules)
+    inst = mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster))
+    rows = workloads.placements(w.seed, args.rows, inst.n_ops, inst.K)
+    dev_rows = torch.from_numpy(rows).cuda()
+    ms = torch.empty(args.rows, dtype=torch.float64, device="cuda")
+    st = torch.empty(args.rows, dtype=torch.int8, device="cuda")
+    stream = torch.cuda.current_stream()
+    lib = N.lib()
+    for G in [int(x) for x in args.G.split(",")]:
+        inst.tune(G, args.ctas_per_sm)
+        info = inst.info()
+        best = C.c_int64()
+        bms = C.c_double()
+        err = N.mp_error()
+
+        def run():
+            code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(dev_rows.data_ptr()), args.rows,
+                                          C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()), C.byref(best),
+                                          C.byref(bms), N.MP_DEVICE_PTRS, C.c_void_p(stream.cuda_stream),
+                                          C.byref(err))
+            N.check(code, err)
+
+        run()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.iters):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        t = min(times)
+        print(f"{w.name} G={G} warps/cta={info['groups_per_cta'] * G // 32} gpc={info['groups_per_cta']} "
+              f"ctas={info['ctas']} rcap={info['ready_cap']} smem={info['smem_bytes']} state={info['state_bytes']} "
+              f"tables={info['table_bytes']}: {args.rows / t:,.0f} placements/s ({t * 1e3:.2f} ms) best={best.value}",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

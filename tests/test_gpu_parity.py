@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's golden
+vectors and, at larger sizes, against the pinned CPU oracle.  Bar: bit-exact
+(fp64 compared as raw bits, placements and partitions compared exactly)."""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import random
+
+import numpy as np
+import pytest
+from conftest import (F, bits, cluster_from, golden, golden_node_tuple, graph_from, mesh_from, node_tuple,
+                      overrides_from, rules_from)
+
+import paper_2312_04025_b200 as mp
+from paper_2312_04025_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+# ---- exact schedules (solver.py:151-165) -------------------------------------------
+def test_schedule_for_assignment_matches_golden():
+    n = 0
+    for case in golden("schedules.json"):
+        g = graph_from(case["graph"])
+        c = cluster_from(case["cluster"])
+        mesh = mesh_from(case["mesh"], c)
+        for asg, want in zip(case["assignments"], case["results"]):
+            a = {int(k): v for k, v in asg.items()}
+            if want["status"] == "memory":
+                with pytest.raises(mp.MemoryExceededError) as ei:
+                    mp.schedule_for_assignment(g, c, mesh, a)
+                assert (ei.value.device, ei.value.overflow) == (want["device"], want["overflow"]), case["name"]
+                continue
+            s = mp.schedule_for_assignment(g, c, mesh, a)
+            assert s.makespan_s.hex() == F(want["makespan"]).hex(), case["name"]
+            assert {k: v.hex() for k, v in s.starts.items()} == {int(k): F(v).hex() for k, v in want["starts"].items()}
+            assert {k: v.hex() for k, v in s.ends.items()} == {int(k): F(v).hex() for k, v in want["ends"].items()}
+            assert s.channels == {int(k): (tuple(v) if v else None) for k, v in want["channels"].items()}
+            assert s.assignment == a
+            n += 1
+    assert n > 300
+
+
+def test_frozen_known_answers():
+    """test_solver.py:155-189 and test_simulator.py:36-47 values."""
+    c = mp.Cluster([mp.Device(0, 100), mp.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
+    mesh = mp.effective_bandwidth(c)
+    g = mp.CompGraph([mp.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}), mp.OpNode(2, "bn", 10, {0: 1.0, 1: 0.5})],
+                     [mp.FlowEdge(1, 2, 10_000_000)])
+    s = mp.schedule_for_assignment(g, c, mesh, {1: 0, 2: 1})
+    assert s.starts == {1: 0.0, 3: 2.0, 2: 4.0} and s.ends == {1: 2.0, 3: 4.0, 2: 4.5}
+    assert s.makespan_s == 4.5 and s.channels == {3: (0, 1)}
+    co = mp.schedule_for_assignment(g, c, mesh, {1: 1, 2: 1})
+    assert co.makespan_s == 4.5 and co.channels == {3: None} and co.starts[3] == co.ends[3] == 4.0
+    c10 = mp.Cluster([mp.Device(0, 10), mp.Device(1, 10)], {(0, 1): 5e6, (1, 0): 5e6})
+    g2 = mp.CompGraph([mp.OpNode(1, "conv", 5, {0: 2.0, 1: 50.0}), mp.OpNode(2, "bn", 5, {0: 3.0, 1: 50.0})], [])
+    s2 = mp.schedule_for_assignment(g2, c10, mp.effective_bandwidth(c10), {1: 0, 2: 0})
+    assert s2.makespan_s == 5.0 and s2.starts[2] == 0.0 and s2.starts[1] == 3.0
+    split = mp.CompGraph([mp.OpNode(1, "conv", 10, {0: 2.0, 1: 100.0}), mp.OpNode(2, "bn", 10, {0: 100.0, 1: 3.0})],
+                         [mp.FlowEdge(1, 2, 100_000_000)])
+    ms, events = mp.simulate(split, c, mesh, {1: 0, 2: 1})
+    assert ms == 25.0
+    assert [(e.time_s, e.kind, e.node, e.device, e.channel) for e in events] == [
+        (0.0, mp.EventKind.OP_START, 1, 0, None), (2.0, mp.EventKind.OP_END, 1, 0, None),
+        (2.0, mp.EventKind.FLOW_START, 3, None, (0, 1)), (22.0, mp.EventKind.OP_START, 2, 1, None),
+        (22.0, mp.EventKind.FLOW_END, 3, None, (0, 1)), (25.0, mp.EventKind.OP_END, 2, 1, None)]
+
+
+def test_errors_match_reference_behaviour():
+    c = mp.Cluster([mp.Device(0, 15), mp.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
+    mesh = mp.effective_bandwidth(c)
+    g = mp.CompGraph([mp.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}), mp.OpNode(2, "bn", 10, {0: 1.0, 1: 0.5})],
+                     [mp.FlowEdge(1, 2, 10_000_000)])
+    with pytest.raises(KeyError):
+        mp.schedule_for_assignment(g, c, mesh, {1: 0})
+    with pytest.raises(KeyError):
+        mp.schedule_for_assignment(g, c, mesh, {1: 0, 2: 9})
+    with pytest.raises(mp.MemoryExceededError) as ei:
+        mp.schedule_for_assignment(g, c, mesh, {1: 0, 2: 0})
+    assert (ei.value.device, ei.value.overflow) == (0, 5)
+    cyc = mp.CompGraph([mp.OpNode(1, "a", 1, {0: 1.0, 1: 1.0}), mp.OpNode(2, "b", 1, {0: 1.0, 1: 1.0})],
+                       [mp.FlowEdge(1, 2, 1), mp.FlowEdge(2, 1, 1)])
+    with pytest.raises(mp.CycleError):
+        mp.schedule_for_assignment(cyc, c, mesh, {1: 0, 2: 0})
+    big = mp.CompGraph([mp.OpNode(i, "c", 1, {k: 1.0 for k in range(4)}) for i in range(1, 14)],
+                       [mp.FlowEdge(i, i + 1, 1) for i in range(1, 13)])
+    c4 = mp.Cluster([mp.Device(k, 100) for k in range(4)], {(a, b): 1e6 for a in range(4) for b in range(4) if a != b})
+    with pytest.raises(mp.TooLargeError):
+        mp.brute_force(big, c4, mp.effective_bandwidth(c4))
+    with pytest.raises(mp.MissingCostError):
+        mp.brute_force(mp.CompGraph([mp.OpNode(1, "c", 1, {0: 1.0})], []), c, mesh)
+    with pytest.raises(ValueError):
+        mp.brute_force(mp.CompGraph([], []), c, mesh)
+
+
+# ---- brute force (solver.py:257-282) ---------------------------------------------------
+def test_brute_force_matches_golden():
+    for case in golden("brute_force.json"):
+        g = graph_from(case["graph"])
+        c = cluster_from(case["cluster"])
+        sol = mp.brute_force(g, c, mp.effective_bandwidth(c))
+        assert sol.status.value == case["status"], case["name"]
+        assert sol.objective_s.hex() == F(case["objective"]).hex(), case["name"]
+        if sol.schedule is not None:
+            assert sol.placement == {int(k): v for k, v in case["placement"].items()}, case["name"]
+            assert sol.schedule.makespan_s == sol.objective_s
+        ex = mp.solve_exact(g, c, mp.effective_bandwidth(c))
+        assert ex.status == sol.status and ex.objective_s == sol.objective_s
+
+
+# ---- GCOF (fusion.py:271-304) ------------------------------------------------------------
+@pytest.mark.parametrize("chunk", range(4))
+def test_gcof_matches_golden(chunk):
+    for case in golden("gcof.json")[chunk::4]:
+        g = graph_from(case["graph"])
+        out = mp.gcof(g, rules_from(case["rules"]), overrides_from(case.get("overrides")))
+        assert [node_tuple(n) for n in out.nodes] == [golden_node_tuple(r) for r in case["out"]["nodes"]], case["name"]
+        assert [[e.src, e.dst, e.payload_bytes] for e in out.edges] == case["out"]["edges"], case["name"]
+
+
+def test_gcof_rejects_cycles_and_is_idempotent():
+    rules = workloads.table_rules()
+    cyc = mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0}), mp.OpNode(2, "bn", 1, {0: 1.0})],
+                       [mp.FlowEdge(1, 2, 1), mp.FlowEdge(2, 1, 1)])
+    with pytest.raises(mp.CycleError):
+        mp.gcof(cyc, rules)
+    for case in golden("gcof.json")[:60]:
+        out = mp.gcof(graph_from(case["graph"]), rules_from(case["rules"]))
+        if case["name"].startswith("random_dag"):
+            assert mp.gcof(out, rules_from(case["rules"])) == out
+
+
+def test_gcof_large_synthetic_vs_oracle(oracle_mod):
+    from paper_2312_04025_b200.fusion import _Flat
+
+    for n, seed in ((5000, 1), (20000, 2)):
+        g = mp.gen_synthetic(mp.GenSpec(ops=n, width=32, density=0.5, devices=(0, 1, 2, 3)), seed)
+        rules = workloads.table_rules()
+        out = mp.gcof(g, rules)
+        k = _Flat(g, rules, None).keep
+        part = oracle_mod.gcof_partition(k[1], k[2], k[3], k[6], k[7], k[10], k[11])
+        nodes, edges = oracle_mod.materialize(g, part)
+        got = [(x.id, x.op_type, x.members, x.type_seq, x.tag.value, x.mem_bytes,
+                {kk: v.hex() for kk, v in x.compute_time.items()}) for x in out.nodes]
+        want = [(i, t, m, s, tg, mem, {kk: float(v).hex() for kk, v in cost.items()})
+                for i, t, m, s, tg, mem, cost in nodes]
+        assert got == want
+        assert [(e.src, e.dst, e.payload_bytes) for e in out.edges] == [tuple(e) for e in edges]
+
+
+# ---- named workloads: coarse graph + makespans vs the reference -------------------------
+def _coarse_sha(g):
+    d = {"nodes": [[n.id, n.op_type, n.mem_bytes, {str(k): float(v).hex() for k, v in n.compute_time.items()},
+                    list(n.members), list(n.type_seq), n.tag.value] for n in g.nodes],
+         "edges": [[e.src, e.dst, e.payload_bytes] for e in g.edges]}
+    return hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()
+
+
+WORKLOADS = {
+    "C1-inception-v4-490ops-K2": workloads.c1,
+    "C2-bert-large-K4": lambda: workloads.c2(4),
+    "C2-bert-large-K8": lambda: workloads.c2(8),
+    "C3-gpt3-96L-K8-48GB": workloads.c3,
+    "C4-vit-large-K8-nvlink": lambda: workloads.c4("nvlink"),
+    "C4-vit-large-K8-pcie": lambda: workloads.c4("pcie"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(WORKLOADS))
+def test_workload_makespans_match_golden(name):
+    rec = next(r for r in golden("workload_evals.json") if r["name"] == name)
+    w = WORKLOADS[name]()
+    coarse = mp.gcof(w.raw, w.rules)
+    assert (len(coarse), len(coarse.edges)) == (rec["n_ops"], rec["n_flows"])
+    assert _coarse_sha(coarse) == rec["coarse_sha256"]
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        rows = workloads.placements(rec["rows_seed"], 16, inst.n_ops, inst.K)
+        ms, st, dev, ov = mp.evaluate_batch(inst, rows, with_detail=True)
+        for k, want in enumerate(rec["results"]):
+            if want["status"] == "memory":
+                assert st[k] == 1 and dev[k] == want["device"] and ov[k] == want["overflow"]
+                assert math.isinf(ms[k])
+            else:
+                assert st[k] == 0 and ms[k].hex() == F(want["makespan"]).hex()
+
+
+# ---- evaluation vs the oracle at scale, every launch shape -------------------------------
+def random_problem(rng, n_ops, k, tight=False, ties=False, zero=False):
+    types = ("conv", "bn", "relu", "add", "matmul", "pool")
+    nodes = []
+    for i in range(1, n_ops + 1):
+        if ties:
+            t = {d: float(rng.choice((1, 2))) for d in range(k)}
+        else:
+            t = {d: round(rng.uniform(0.5, 8.0), 3) for d in range(k)}
+        if zero and rng.random() < 0.2:
+            t = {d: 0.0 for d in range(k)}
+        nodes.append(mp.OpNode(i, rng.choice(types), rng.randint(1, 40 if tight else 10), t))
+    edges = []
+    for j in range(2, n_ops + 1):
+        preds = [i for i in range(max(1, j - 12), j) if rng.random() < 0.3]
+        if not preds and rng.random() < 0.8:
+            preds = [rng.randint(1, j - 1)]
+        for i in preds:
+            edges.append(mp.FlowEdge(i, j, (10_000_000 if ties else rng.randint(1_000_000, 30_000_000))
+                                     * (0 if zero and rng.random() < 0.1 else 1)))
+    g = mp.CompGraph(nodes, edges)
+    cap = 80 * n_ops // 6 if tight else 10 ** 9
+    links = {(a, b): (1e7 if ties else rng.uniform(4e6, 4e7)) for a in range(k) for b in range(k) if a != b}
+    return g, mp.Cluster([mp.Device(d, cap) for d in range(k)], links)
+
+
+SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (2, 4, 8, 16, 32) for colo in (True, False)
+          for rc in (0, 3)]
+
+
+@pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
+def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
+    rng = random.Random({"plain": 1, "tight": 2, "ties": 3, "zero": 4}[flavor])
+    for trial in range(6):
+        g, c = random_problem(rng, rng.randint(3, 60), rng.randint(2, 5), tight=flavor == "tight",
+                              ties=flavor == "ties", zero=flavor == "zero")
+        with mp.Instance(g, c, mp.effective_bandwidth(c)) as inst:
+            orc = oracle_mod.OracleInstance.from_instance(inst)
+            rows = np.random.default_rng(trial).integers(0, inst.K, (300, inst.n_ops), dtype=np.uint8)
+            want, wst = orc.eval_batch(rows)
+            feas = np.where(wst == 0)[0]
+            want_best = int(feas[np.argmin(want[feas])]) if len(feas) else -1
+            for shape in SHAPES:
+                inst.tune(**shape)
+                ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
+                assert np.array_equal(st, wst), (flavor, trial, shape)
+                assert np.array_equal(bits(ms), bits(want)), (flavor, trial, shape, inst.info())
+                best, bms = mp.argmin(inst, rows)
+                assert best == want_best, (flavor, trial, shape)
+            if flavor == "zero":
+                assert inst.info()["colo_ok"] in (0, 1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
+def test_eval_vs_oracle_workloads(oracle_mod, name):
+    w = {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c4": workloads.c4,
+         "c5": lambda: workloads.c5(2000, 4)}[name]()
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        rows = workloads.placements(w.seed, 4096 if name != "c5" else 256, inst.n_ops, inst.K)
+        want, wst = orc.eval_batch(rows, threads=8)
+        for shape in (dict(), dict(group_lanes=8), dict(group_lanes=32, colo=False)):
+            inst.tune(**shape)
+            ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
+            assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)
+
+
+def test_trace_matches_oracle_on_workload(oracle_mod):
+    w = workloads.c2(8)
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        for row in workloads.placements(9, 8, inst.n_ops, inst.K):
+            s = mp.solver._schedule_row(inst, row)
+            _, oms, ost, oen, _, _ = orc.schedule(row)
+            ids = inst.op_ids + [inst.flow_id(f) for f in range(inst.n_flows)]
+            assert np.array_equal(bits([s.starts[i] for i in ids]), bits(ost))
+            assert np.array_equal(bits([s.ends[i] for i in ids]), bits(oen))
+            assert s.makespan_s == oms
+
+
+def test_device_pointer_path_and_chunking():
+    """Host-pointer calls are chunked; results equal the device-pointer call."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2312_04025_b200 import _native as N
+
+    w = workloads.c2(4)
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        rows = workloads.placements(2, 50_001, inst.n_ops, inst.K)
+        host_ms = mp.evaluate_batch(inst, rows)
+        d_rows = torch.from_numpy(rows).cuda()
+        d_ms = torch.empty(len(rows), dtype=torch.float64, device="cuda")
+        err = N.mp_error()
+        code = inst._lib.mp_evaluate_batch(inst.handle, C.c_void_p(d_rows.data_ptr()), len(rows),
+                                           C.c_void_p(d_ms.data_ptr()), None, None, None, N.MP_DEVICE_PTRS,
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(err))
+        N.check(code, err)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(d_ms.cpu().numpy()), bits(host_ms))
+
+
+# ---- local search (K5): every reported placement re-verifies bit-exactly -----------------
+def test_local_search_reverifies_and_is_deterministic(oracle_mod):
+    w = workloads.c2(4)
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        seeds = workloads.placements(2, 16, inst.n_ops, inst.K)
+        seed_ms = mp.evaluate_batch(inst, seeds)
+        a = mp.local_search(inst, seeds, chains=512, moves=48, seed=7)
+        inst.tune(group_lanes=8, colo=False)
+        b = mp.local_search(inst, seeds, chains=512, moves=48, seed=7)
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1] and a[2] == b[2]
+        assert np.array_equal(bits(a[3]), bits(b[3]))
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        st, oms, *_ = orc.schedule(a[0])
+        assert st == 0 and oms == a[1]
+        assert a[1] <= seed_ms.min()
+        assert a[1] == a[3].min()
