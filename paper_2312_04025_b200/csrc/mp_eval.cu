@@ -454,8 +454,8 @@ template <int G, int SRC, bool ONCHIP, bool TRACE, bool COLO>
 __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
-    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 4];
-    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 4];
+    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 2];
+    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 2];
     constexpr int GPW = 32 / G;  // groups per warp
 
     const int lane = threadIdx.x & 31;
