@@ -88,6 +88,7 @@ typedef struct mp_instance_info {
     int32_t n_sources;
     int32_t ready_cap;          /* on-chip ready-set capacity per placement          */
     int32_t group_lanes;        /* lanes cooperating on one placement (G)            */
+    int32_t lanes_used;         /* lanes per warp owning a placement (U)             */
     int32_t groups_per_cta;
     int32_t ctas;               /* persistent grid size                              */
     int32_t smem_bytes;         /* dynamic shared memory per CTA                     */
@@ -112,11 +113,13 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device,
                            mp_instance **out, mp_error *err);
 void    mp_instance_destroy(mp_instance *inst);
 int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
-/* Override the launch shape: lanes per placement G in {2,4,8,16,32} (0 = auto),
- * CTAs per SM cap (0 = auto), on-chip ready capacity (0 = auto); flags bit 0
- * (MP_TUNE_NO_COLO) dispatches co-located flows as ordinary steps. */
+/* Override the launch shape: lanes per placement G in {1,2,4,8,16,32} (0 = auto),
+ * lanes per warp that own a placement U (multiple of G, <= 32; 0 = auto), CTAs
+ * per SM cap (0 = auto), on-chip ready capacity (0 = auto); flags bit 0
+ * (MP_TUNE_NO_COLO) dispatches co-located flows as ordinary steps.  Results
+ * never depend on these knobs. */
 #define MP_TUNE_NO_COLO 1
-int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t ctas_per_sm,
+int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,
                          int32_t ready_cap, uint32_t flags);
 
 /* ---- batched evaluation (K3; replaces one `_schedule` call per row) ------ */

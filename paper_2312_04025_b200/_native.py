@@ -52,7 +52,8 @@ class mp_instance_info(C.Structure):
     _fields_ = [
         ("n_ops", C.c_int32), ("n_flows", C.c_int32), ("n_dev", C.c_int32),
         ("n_levels", C.c_int32), ("n_sources", C.c_int32), ("ready_cap", C.c_int32),
-        ("group_lanes", C.c_int32), ("groups_per_cta", C.c_int32), ("ctas", C.c_int32),
+        ("group_lanes", C.c_int32), ("lanes_used", C.c_int32), ("groups_per_cta", C.c_int32),
+        ("ctas", C.c_int32),
         ("smem_bytes", C.c_int32), ("onchip", C.c_int32), ("device", C.c_int32),
         ("n_multi", C.c_int32), ("ready_bound", C.c_int32), ("colo", C.c_int32), ("colo_ok", C.c_int32),
         ("table_bytes", C.c_int64), ("state_bytes", C.c_int64),
@@ -92,7 +93,7 @@ SIGNATURES = {
                                         C.POINTER(mp_error)]),
     "mp_instance_destroy": (None, [C.c_void_p]),
     "mp_instance_info_get": (C.c_int32, [C.c_void_p, C.POINTER(mp_instance_info)]),
-    "mp_instance_tune": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_uint32]),
+    "mp_instance_tune": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint32]),
     "mp_evaluate_batch": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
                                        C.POINTER(mp_error)]),

@@ -92,6 +92,8 @@ struct EvalArgs {
     unsigned long long *next;     // work counter (rows handed out)
     unsigned char *gstate;        // global-state slots (off-chip mode)
     int groups_per_cta;
+    int lanes_used;               // U: lanes per warp that own a group (multiple of G); the
+                                  // rest idle on a shared dummy slot (slot index groups_per_cta)
     int want_argmin;
     int row_list;                 // 1: `row_idx` lists the global rows to (re)evaluate
     const long long *row_idx;     // [n_rows] global row indices (row_list mode)
@@ -166,6 +168,7 @@ __device__ __forceinline__ bool key_less(unsigned long long e, unsigned long lon
 // ---- host-side launch plumbing (mp_eval.cu) ---------------------------------
 struct LaunchShape {
     int G;                // lanes per placement
+    int U;                // lanes per warp owning a group
     int groups_per_cta;
     int threads;
     int ctas;

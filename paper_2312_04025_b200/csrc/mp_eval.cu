@@ -92,6 +92,13 @@ __device__ __forceinline__ T *slot(unsigned char *st, uint32_t off) {
     return reinterpret_cast<T *>(st + off);
 }
 
+// (e, -rank, id) lexicographic "less" without short-circuit branches.
+__device__ __forceinline__ bool key_less_nb(unsigned long long e, unsigned long long r, uint32_t n,
+                                            unsigned long long be, unsigned long long br, uint32_t bn) {
+    const bool elt = e < be, eeq = e == be, rgt = r > br, req = r == br, nlt = n < bn;
+    return elt | (eeq & (rgt | (req & nlt)));
+}
+
 struct RowResult {
     double ms;
     int status;      // MP_ROW_* or MP_ROW_OVERFLOW
@@ -173,6 +180,16 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     const bool alive = live && res.status == MP_ROW_OK;
     __syncwarp();
 
+    // table bases (hoisted: one address computation per kernel, not per access)
+    const double *__restrict__ T_cost = tab<double>(tb, a.to.cost);
+    const double *__restrict__ T_bw = tab<double>(tb, a.to.bw);
+    const uint32_t *__restrict__ T_out_beg = tab<uint32_t>(tb, a.to.out_beg);
+    const uint32_t *__restrict__ T_s_dst = tab<uint32_t>(tb, a.to.s_dst);
+    const uint32_t *__restrict__ T_s_fid = tab<uint32_t>(tb, a.to.s_fid);
+    const double *__restrict__ T_s_pay = tab<double>(tb, a.to.s_pay);
+    const uint32_t *__restrict__ T_fdst = tab<uint32_t>(tb, a.to.fdst);
+    const uint32_t *__restrict__ T_mi = tab<uint32_t>(tb, a.to.mi);
+
     // ---- 2+3. durations folded into the rank pass (solver.py:89-107) ------------
     double *rank = slot<double>(st, a.so.rank);
     for (int lv = 0; lv < a.n_levels; ++lv) {
@@ -182,16 +199,17 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int i = static_cast<int>(tab<uint32_t>(tb, a.to.lvl_ops)[t]);
             const int d = dev[i];
             double best = 0.0;
-            const int qe = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[i + 1]);
-            for (int q = static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[i]); q < qe; ++q) {
-                const int j = static_cast<int>(tab<uint32_t>(tb, a.to.s_dst)[q]);
+            const int qe = static_cast<int>(T_out_beg[i + 1]);
+            for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
+                const int j = static_cast<int>(T_s_dst[q]);
                 const int dj = dev[j];
                 // rank of the flow node = dur + rank[j]   (rank[j] >= +0.0)
-                double fr = rank[j];
-                if (dj != d) fr = tab<double>(tb, a.to.s_pay)[q] / tab<double>(tb, a.to.bw)[d * K + dj] + fr;
-                if (fr > best) best = fr;
+                const bool cross = dj != d;
+                const double dv = T_s_pay[q] / (cross ? T_bw[d * K + dj] : 1.0);
+                const double fr = cross ? dv + rank[j] : rank[j];
+                best = fr > best ? fr : best;
             }
-            rank[i] = tab<double>(tb, a.to.cost)[i * K + d] + best;
+            rank[i] = T_cost[i * K + d] + best;
         }
         __syncwarp();
     }
@@ -211,6 +229,14 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         m_tie[k] = tab<uint32_t>(tb, a.to.m_op)[k];
     }
     for (int k = gl; k <= static_cast<int>(WS); k += G) clk[k] = 0.0;
+    if (gl == 0) {  // the branch-free scan may read entry 0 of an empty ready set
+        r_meta[0] = (RZ << 20) | (RZ << 26);
+        r_est[0] = 0.0;
+        r_rank[0] = 0.0;
+        r_dur[0] = 0.0;
+        r_tie[0] = 0;
+    }
+    __syncwarp();
     int nready = a.n_src;
     bool ovf = alive && nready > rcap;
     if (alive && !ovf) {
@@ -219,7 +245,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int d = dev[i];
             r_est[t] = 0.0;
             r_rank[t] = rank[i];
-            r_dur[t] = tab<double>(tb, a.to.cost)[i * K + d];
+            r_dur[t] = T_cost[i * K + d];
             r_meta[t] = static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26);
             r_tie[t] = static_cast<uint32_t>(i);
         }
@@ -229,7 +255,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     bool done = !alive || ovf;
     double ms = 0.0;
     while (__any_sync(kFull, !done)) {
-        // -- local minimum over this lane's slice of the ready set ----------------
+        // -- local minimum over this lane's slice of the ready set (branch-free) ---
         const int maxr = __reduce_max_sync(kFull, done ? 0 : nready);
         unsigned long long be = ~0ULL, br = 0ULL;
         uint32_t bi = 0xffffffffu, bmeta = 0;
@@ -237,24 +263,25 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         int bs = -1;
         for (int s0 = 0; s0 < maxr; s0 += G) {
             const int s = s0 + gl;
-            if (!done && s < nready) {
-                const uint32_t m = r_meta[s];
-                const unsigned long long es = dbits(r_est[s]);
-                const unsigned long long c1 = dbits(clk[(m >> 20) & 63u]);
-                const unsigned long long c2 = dbits(clk[m >> 26]);
-                unsigned long long e = es > c1 ? es : c1;
-                e = e > c2 ? e : c2;
-                const unsigned long long r = dbits(r_rank[s]);
-                const uint32_t id = (COLO && e == es) ? r_tie[s] : (m & MP_NODE_MASK);
-                if (key_less(e, r, id, be, br, bi)) {
-                    be = e;
-                    br = r;
-                    bi = id;
-                    bmeta = m;
-                    bdur = r_dur[s];
-                    bs = s;
-                }
-            }
+            const bool valid = !done && s < nready;
+            const int sc = valid ? s : 0;  // slot arrays always hold >= 1 entry
+            const uint32_t m = r_meta[sc];
+            const unsigned long long es = dbits(r_est[sc]);
+            const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
+            const unsigned long long c1 = dbits(clk[i1 <= WS ? i1 : RZ]);
+            const unsigned long long c2 = dbits(clk[i2 <= WS ? i2 : RZ]);
+            unsigned long long e = es > c1 ? es : c1;
+            e = e > c2 ? e : c2;
+            const unsigned long long r = dbits(r_rank[sc]);
+            const uint32_t id = (COLO && e == es) ? r_tie[sc] : (m & MP_NODE_MASK);
+            const double du = r_dur[sc];
+            const bool take = valid & key_less_nb(e, r, id, be, br, bi);
+            be = take ? e : be;
+            br = take ? r : br;
+            bi = take ? id : bi;
+            bmeta = take ? m : bmeta;
+            bdur = take ? du : bdur;
+            bs = take ? s : bs;
         }
         const uint32_t mine = bi;
         // -- G-lane butterfly: every lane ends with its group's minimum -----------
@@ -263,11 +290,10 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const unsigned long long e2 = __shfl_xor_sync(kFull, be, o, G);
             const unsigned long long r2 = __shfl_xor_sync(kFull, br, o, G);
             const uint32_t i2 = __shfl_xor_sync(kFull, bi, o, G);
-            if (key_less(e2, r2, i2, be, br, bi)) {
-                be = e2;
-                br = r2;
-                bi = i2;
-            }
+            const bool take = key_less_nb(e2, r2, i2, be, br, bi);
+            be = take ? e2 : be;
+            br = take ? r2 : br;
+            bi = take ? i2 : bi;
         }
         // -- the owning lane broadcasts the winner's meta / duration --------------
         const bool owner = !done && bs >= 0 && mine == bi;
@@ -284,7 +310,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             r_tie[bs] = r_tie[last];
         }
         __syncwarp();
-        if (!done) nready = last;
+        nready = done ? nready : last;
 
         // -- commit (solver.py:130-138): start = e, end = e + dur ----------------
         const double E = bitsd(be);
@@ -300,106 +326,77 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
                 a.ends[node] = end;
             }
         }
-        if (!done && isop && end > ms) ms = end;
+        ms = (!done && isop && end > ms) ? end : ms;
 
         // -- successors (solver.py:140-145) ---------------------------------------
         // op    -> its out-flows (crossing ones enter the ready set; co-located ones
         //          update their consumer directly in colo mode)
         // flow  -> its destination op (npred-- / est max / maybe ready)
-        const int d = isop ? static_cast<int>(r1) : 0;
-        const int ob = (!done && isop) ? static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node]) : 0;
-        const int cnt = done ? 0 : (isop ? static_cast<int>(tab<uint32_t>(tb, a.to.out_beg)[node + 1]) - ob : 1);
+        // Computed branch-free with clamped indices; only the stores are predicated.
+        const int d = static_cast<int>(r1);  // op: its device (unused for flows)
+        const int nodec = done ? 0 : node;
+        const int ob = static_cast<int>(T_out_beg[isop ? nodec : 0]);
+        const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
+        const uint32_t jflow = T_fdst[isop ? 0 : node - n_ops];
         const int maxc = __reduce_max_sync(kFull, cnt);
         for (int t0 = 0; t0 < maxc; t0 += G) {
             const int t = t0 + gl;
-            bool ins = false;
-            double ne = 0.0, nr = 0.0, nd = 0.0;
-            uint32_t nm = 0, nt = 0;
-            if (t < cnt) {
-                int j;           // the op that may become ready
-                uint32_t pid;    // node id of the pred flow updating it
-                bool via_colo = false;
-                bool op_update = true;
-                if (isop) {
-                    const int q = ob + t;
-                    j = static_cast<int>(tab<uint32_t>(tb, a.to.s_dst)[q]);
-                    const int dj = dev[j];
-                    pid = static_cast<uint32_t>(n_ops) + tab<uint32_t>(tb, a.to.s_fid)[q];
-                    if (COLO && dj == d) {
-                        via_colo = true;  // zero-duration flow: start = end = producer's end
-                        if constexpr (TRACE) {
-                            a.starts[pid] = end;
-                            a.ends[pid] = end;
-                        }
-                    } else {
-                        op_update = false;
-                        double dur = 0.0;
-                        uint32_t m = pid;
-                        if (dj != d) {
-                            dur = tab<double>(tb, a.to.s_pay)[q] / tab<double>(tb, a.to.bw)[d * K + dj];
-                            m |= (static_cast<uint32_t>(K + d) << 20) | (static_cast<uint32_t>(2 * K + dj) << 26);
-                        } else {
-                            m |= (RZ << 20) | (RZ << 26);
-                        }
-                        ins = true;
-                        ne = end;
-                        nr = dur + rank[j];
-                        nd = dur;
-                        nm = m;
-                        nt = pid;
-                    }
-                } else {
-                    j = static_cast<int>(tab<uint32_t>(tb, a.to.fdst)[node - n_ops]);
-                    pid = static_cast<uint32_t>(node);
-                }
-                if (op_update) {
-                    const uint32_t k = tab<uint32_t>(tb, a.to.mi)[j];
-                    bool ready = true;
-                    double ej = end;
-                    uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
-                    if (k != MP_NONE) {
-                        const int np = static_cast<int>(m_np[k]) - 1;
-                        m_np[k] = static_cast<uint16_t>(np);
-                        const double cur = m_est[k];
-                        uint32_t ct = m_tie[k];
-                        if (end > cur) {
-                            m_est[k] = end;
-                            ct = tj;
-                        } else {
-                            ej = cur;
-                            if (via_colo && end == cur && pid > ct) ct = pid;
-                        }
-                        m_tie[k] = ct;
-                        tj = ct;
-                        ready = np == 0;
-                    }
-                    if (ready) {
-                        const int dj = dev[j];
-                        ins = true;
-                        ne = ej;
-                        nr = rank[j];
-                        nd = tab<double>(tb, a.to.cost)[j * K + dj];
-                        nm = static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26);
-                        nt = tj;
-                    }
-                }
+            const bool act = t < cnt;
+            const int q = (act && isop) ? ob + t : 0;
+            const int j = static_cast<int>(isop ? T_s_dst[q] : jflow);
+            const int dj = dev[j];
+            const uint32_t pid = isop ? static_cast<uint32_t>(n_ops) + T_s_fid[q] : static_cast<uint32_t>(node);
+            const bool cross = dj != d;
+            const bool via_colo = COLO && isop && !cross;
+            const bool flow_ins = act && isop && !via_colo;   // a flow enters the ready set
+            const bool op_upd = act && !flow_ins;             // j's npred / est / gate change
+            // flow entry (crossing: payload / bw; co-located without colo: 0.0)
+            const bool fcross = isop && cross;
+            const double fdur = fcross ? T_s_pay[q] / T_bw[fcross ? d * K + dj : 0] : 0.0;
+            const double rj = rank[j];
+            const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                   (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                : ((RZ << 20) | (RZ << 26)));
+            // op update: multi-input ops keep npred / est / gate id
+            const uint32_t k = T_mi[j];
+            const bool multi = k != MP_NONE;
+            const uint32_t kc = multi ? k : 0;
+            const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+            const int np = static_cast<int>(m_np[kc]) - 1;
+            const double cur = m_est[kc];
+            const uint32_t ct = m_tie[kc];
+            const bool up = end > cur;
+            const double ej = multi ? (up ? end : cur) : end;
+            const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
+            const uint32_t tie_j = multi ? tie_new : tj;
+            if (op_upd && multi) {
+                m_np[kc] = static_cast<uint16_t>(np);
+                m_est[kc] = ej;
+                m_tie[kc] = tie_new;
             }
+            const bool op_ins = op_upd && (!multi || np == 0);
+            const bool ins = flow_ins || op_ins;
+            const double odur = T_cost[j * K + dj];
             const unsigned bal = __ballot_sync(kFull, ins);
             const int pos = nready + __popc(bal & below);
             if (ins && pos < rcap) {
-                r_est[pos] = ne;
-                r_rank[pos] = nr;
-                r_dur[pos] = nd;
-                r_meta[pos] = nm;
-                r_tie[pos] = nt;
+                r_est[pos] = flow_ins ? end : ej;
+                r_rank[pos] = flow_ins ? fdur + rj : rj;
+                r_dur[pos] = flow_ins ? fdur : odur;
+                r_meta[pos] = flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26));
+                r_tie[pos] = flow_ins ? pid : tie_j;
+            }
+            if constexpr (TRACE) {
+                if (act && via_colo) {  // zero-duration flow: start = end = producer's end
+                    a.starts[pid] = end;
+                    a.ends[pid] = end;
+                }
             }
             nready += __popc(bal & gbits);
         }
-        if (!done && nready > rcap) {
-            ovf = true;
-            done = true;
-        }
-        if (!done && nready == 0) done = true;  // every node committed
+        const bool over = !done && nready > rcap;
+        ovf = ovf || over;
+        done = done || over || nready == 0;  // nready == 0: every node committed
         __syncwarp();
     }
     if (!alive) return res;
@@ -411,19 +408,30 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     return res;
 }
 
-template <int G>
-__device__ __forceinline__ void cta_keep_best(const EvalArgs &a, double best_ms, long long best_row, int gl, int grp,
-                                              double *s_ms, long long *s_row) {
-    if (gl == 0) {
-        s_ms[grp] = best_ms;
-        s_row[grp] = best_row;
+// Per-CTA keep-best: lexicographic (makespan, row) minimum over every lane
+// (lanes of a group agree; idle lanes carry +inf), merged into the CTA's
+// running record in global memory.
+__device__ __forceinline__ void cta_keep_best(const EvalArgs &a, double best_ms, long long best_row, double *s_ms,
+                                              long long *s_row) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double m2 = __shfl_xor_sync(kFull, best_ms, o);
+        const long long r2 = __shfl_xor_sync(kFull, best_row, o);
+        if (m2 < best_ms || (m2 == best_ms && r2 < best_row)) {
+            best_ms = m2;
+            best_row = r2;
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_ms[w] = best_ms;
+        s_row[w] = best_row;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double bm = a.cta_best_ms[blockIdx.x];
         long long brow = a.cta_best_row[blockIdx.x];
-        const int ng = blockDim.x / G;
-        for (int g = 0; g < ng; ++g) {
+        for (int g = 0; g < static_cast<int>(blockDim.x >> 5); ++g) {
             if (s_ms[g] < bm || (s_ms[g] == bm && s_row[g] < brow)) {
                 bm = s_ms[g];
                 brow = s_row[g];
@@ -434,6 +442,7 @@ __device__ __forceinline__ void cta_keep_best(const EvalArgs &a, double best_ms,
     }
 }
 
+// grp == groups_per_cta is the dummy slot shared by idle lanes (lane >= U).
 template <bool ONCHIP>
 __device__ __forceinline__ void group_bases(unsigned char *sm, const EvalArgs &a, int grp, uint64_t *bar,
                                             const unsigned char *&tb, unsigned char *&st) {
@@ -443,8 +452,14 @@ __device__ __forceinline__ void group_bases(unsigned char *sm, const EvalArgs &a
         st = sm + a.to.bytes + static_cast<size_t>(grp) * a.so.bytes;
     } else {
         tb = a.blob;
-        st = a.gstate + (static_cast<size_t>(blockIdx.x) * a.groups_per_cta + grp) * a.so.bytes;
+        st = a.gstate + (static_cast<size_t>(blockIdx.x) * (a.groups_per_cta + 1) + grp) * a.so.bytes;
     }
+}
+
+template <int G>
+__device__ __forceinline__ int group_of_lane(const EvalArgs &a, int lane, bool &idle) {
+    idle = lane >= a.lanes_used;
+    return idle ? a.groups_per_cta : (threadIdx.x >> 5) * (a.lanes_used / G) + lane / G;
 }
 
 }  // namespace
@@ -454,13 +469,13 @@ template <int G, int SRC, bool ONCHIP, bool TRACE, bool COLO>
 __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
-    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 2];
-    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 2];
-    constexpr int GPW = 32 / G;  // groups per warp
-
+    __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 32];
+    __shared__ long long s_best_row[MP_CTA_MAX_THREADS / 32];
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
-    const int grp = threadIdx.x / G;
+    bool idle;
+    const int grp = group_of_lane<G>(a, lane, idle);
+    const int GPW = a.lanes_used / G;  // groups per warp
     const unsigned char *tb;
     unsigned char *st;
     group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
@@ -476,7 +491,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __gri
         base = __shfl_sync(kFull, base, 0);
         if (base >= static_cast<unsigned long long>(n_rows)) break;
         const unsigned long long p = base + static_cast<unsigned long long>(lane / G);
-        const bool live = p < static_cast<unsigned long long>(n_rows);
+        const bool live = !idle && p < static_cast<unsigned long long>(n_rows);
 
         long long grow = 0;  // global row / enumeration index
         unsigned char *dev;
@@ -518,7 +533,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __gri
         }
         __syncwarp();
     }
-    if (a.want_argmin) cta_keep_best<G>(a, best_ms, best_row, gl, grp, s_best_ms, s_best_row);
+    if (a.want_argmin) cta_keep_best(a, best_ms, best_row, s_best_ms, s_best_row);
 }
 
 // ---- K5: local search ---------------------------------------------------------------
@@ -541,10 +556,11 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_ls_kernel(const __grid_
                                                                      const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
-    constexpr int GPW = 32 / G;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
-    const int grp = threadIdx.x / G;
+    bool idle;
+    const int grp = group_of_lane<G>(a, lane, idle);
+    const int GPW = a.lanes_used / G;
     const unsigned char *tb;
     unsigned char *st;
     group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
@@ -557,7 +573,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_ls_kernel(const __grid_
         base = __shfl_sync(kFull, base, 0);
         if (base >= static_cast<unsigned long long>(ls.n_chains)) break;
         const unsigned long long c = base + static_cast<unsigned long long>(lane / G);
-        const bool live = c < static_cast<unsigned long long>(ls.n_chains);
+        const bool live = !idle && c < static_cast<unsigned long long>(ls.n_chains);
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
         if (live) {
             const uint8_t *seed = ls.seed_rows + (gc % static_cast<unsigned long long>(ls.n_seed)) * n;
@@ -676,6 +692,7 @@ EvalFn pick_g(int src, bool onchip, bool trace) {
 template <bool COLO>
 EvalFn pick_c(int G, int src, bool onchip, bool trace) {
     switch (G) {
+        case 1: return pick_g<1, COLO>(src, onchip, trace);
         case 2: return pick_g<2, COLO>(src, onchip, trace);
         case 4: return pick_g<4, COLO>(src, onchip, trace);
         case 8: return pick_g<8, COLO>(src, onchip, trace);
@@ -691,6 +708,7 @@ EvalFn pick_any(int G, int src, bool onchip, bool trace, bool colo) {
 template <bool COLO>
 LsFn pick_ls_c(int G, bool onchip) {
     switch (G) {
+        case 1: return onchip ? mp_ls_kernel<1, true, COLO> : mp_ls_kernel<1, false, COLO>;
         case 2: return onchip ? mp_ls_kernel<2, true, COLO> : mp_ls_kernel<2, false, COLO>;
         case 4: return onchip ? mp_ls_kernel<4, true, COLO> : mp_ls_kernel<4, false, COLO>;
         case 8: return onchip ? mp_ls_kernel<8, true, COLO> : mp_ls_kernel<8, false, COLO>;
@@ -705,8 +723,8 @@ LsFn pick_ls(int G, bool onchip, bool colo) { return colo ? pick_ls_c<true>(G, o
 cudaError_t mp_eval_set_smem_limits() {
     static bool done = false;
     if (done) return cudaSuccess;
-    const int Gs[5] = {2, 4, 8, 16, 32};
-    for (int gi = 0; gi < 5; ++gi) {
+    const int Gs[6] = {1, 2, 4, 8, 16, 32};
+    for (int gi = 0; gi < 6; ++gi) {
         for (int colo = 0; colo < 2; ++colo) {
             for (int src = 0; src < 2; ++src) {
                 EvalFn f = pick_any(Gs[gi], src, true, false, colo != 0);

@@ -233,7 +233,7 @@ StOff make_stoff(int n_ops, int n_multi, int K, int rcap) {
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) {
         const uint32_t at = static_cast<uint32_t>(o);
-        o = align16(o + bytes);
+        o = align16(o + std::max<uint64_t>(bytes, 16));
         return at;
     };
     s.rank = take(8ULL * n_ops);
@@ -256,7 +256,7 @@ TabOff make_taboff(int n_ops, int n_flows, int K) {
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) {
         const uint32_t at = static_cast<uint32_t>(o);
-        o = align16(o + bytes);
+        o = align16(o + std::max<uint64_t>(bytes, 16));
         return at;
     };
     t.cost = take(8ULL * n_ops * K);
@@ -329,30 +329,40 @@ struct mp_instance {
 
 namespace {
 
-void choose_shapes(mp_instance *I, int G_req, int ctas_per_sm_req) {
+void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     const int n_ops = I->n_ops, K = I->K;
     const int smem_cap = MP_SMEM_DYN_MAX;
     // Ready sets are antichains of the augmented DAG, so a vertex-disjoint path
     // cover bounds them: every non-sink op continues into one out-flow and every
     // non-source op is continued by one in-flow -> n_flows - n_ops + n_src + n_sinks
-    // paths.  On chip the capacity is min(bound, 32): rows whose ready set
+    // paths.  On chip the capacity is min(bound, target): rows whose ready set
     // outgrows it are re-run by the off-chip variant with capacity = bound.
     int rcap = std::max(1, std::min(I->ready_bound, I->rcap_target));
     StOff so = make_stoff(n_ops, I->n_multi, K, rcap);
-    int G = G_req > 0 ? G_req : (I->ready_bound <= 16 ? 4 : 8);
-    const int per_warp = 32 / G;
+    const int G = G_req > 0 ? G_req : (I->ready_bound <= 16 ? 4 : 8);
+    // slots that fit next to the tables (one extra dummy slot for idle lanes)
     const long long avail = static_cast<long long>(smem_cap) - I->to.bytes;
-    long long groups_fit = avail > 0 ? avail / so.bytes : 0;
-    int warps = static_cast<int>(std::min<long long>(groups_fit / per_warp, MP_CTA_MAX_THREADS / 32));
-    if (warps >= 1) {
+    const long long slots = avail > 0 ? avail / so.bytes - 1 : 0;
+    int best_U = 0, best_w = 0;
+    for (int U = 32; U >= G; U /= 2) {
+        if (U_req > 0 && U != U_req) continue;
+        const int gpw = U / G;
+        const int w = static_cast<int>(std::min<long long>(slots / gpw, MP_CTA_MAX_THREADS / 32));
+        if (w >= 1 && static_cast<long long>(w) * gpw > static_cast<long long>(best_w) * (best_U / G ? best_U / G : 1)) {
+            best_U = U;
+            best_w = w;
+        }
+    }
+    if (best_w >= 1) {
         LaunchShape ls{};
         ls.G = G;
-        ls.threads = warps * 32;
-        ls.groups_per_cta = ls.threads / G;
-        ls.smem = static_cast<int>(I->to.bytes + static_cast<long long>(ls.groups_per_cta) * so.bytes);
+        ls.U = best_U;
+        ls.threads = best_w * 32;
+        ls.groups_per_cta = best_w * (best_U / G);
+        ls.smem = static_cast<int>(I->to.bytes + static_cast<long long>(ls.groups_per_cta + 1) * so.bytes);
         ls.onchip = true;
-        // static smem of the kernel is ~2 KB; 228 KB per SM in total
-        int per_sm = std::max(1, (228 * 1024) / (ls.smem + 3 * 1024));
+        // static smem of the kernel is ~9 KB; 228 KB per SM in total
+        int per_sm = std::max(1, (228 * 1024) / (ls.smem + 10 * 1024));
         per_sm = std::min(per_sm, 2048 / ls.threads);
         if (ctas_per_sm_req > 0) per_sm = std::min(per_sm, ctas_per_sm_req);
         ls.ctas = I->sms * per_sm;
@@ -366,6 +376,7 @@ void choose_shapes(mp_instance *I, int G_req, int ctas_per_sm_req) {
     StOff wso = make_stoff(n_ops, I->n_multi, K, std::max(1, I->ready_bound));
     LaunchShape w{};
     w.G = 32;
+    w.U = 32;
     w.threads = 256;
     w.groups_per_cta = 8;
     w.onchip = false;
@@ -398,6 +409,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.colo = I->colo ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
+    a.lanes_used = wide ? I->wide.U : I->main.U;
     a.gstate = static_cast<unsigned char *>(wide ? I->wide_state.p : I->main_state.p);
     return a;
 }
@@ -651,7 +663,7 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         I->colo = ok;
     }
 
-    choose_shapes(I, 0, 0);
+    choose_shapes(I, 0, 0, 0);
     *out = I;
     return MP_OK;
 #undef MP_CUDA_I
@@ -681,6 +693,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->n_sources = I->n_src;
     info->ready_cap = I->main_rcap;
     info->group_lanes = I->main.G;
+    info->lanes_used = I->main.U;
     info->groups_per_cta = I->main.groups_per_cta;
     info->ctas = I->main.ctas;
     info->smem_bytes = I->main.onchip ? I->main.smem : 0;
@@ -695,17 +708,20 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     return MP_OK;
 }
 
-int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t ctas_per_sm, int32_t ready_cap,
-                         uint32_t flags) {
+int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,
+                         int32_t ready_cap, uint32_t flags) {
     if (!I) return MP_ERR_INVALID;
-    if (group_lanes != 0 && group_lanes != 2 && group_lanes != 4 && group_lanes != 8 && group_lanes != 16 &&
-        group_lanes != 32)
+    if (group_lanes != 0 && group_lanes != 1 && group_lanes != 2 && group_lanes != 4 && group_lanes != 8 &&
+        group_lanes != 16 && group_lanes != 32)
+        return MP_ERR_INVALID;
+    if (lanes_used < 0 || lanes_used > 32 || (lanes_used & (lanes_used - 1)) != 0 ||
+        (lanes_used && group_lanes && lanes_used < group_lanes))
         return MP_ERR_INVALID;
     if (ready_cap < 0 || ctas_per_sm < 0) return MP_ERR_INVALID;
     std::lock_guard<std::mutex> lk(I->mu);
     I->rcap_target = ready_cap > 0 ? ready_cap : 32;
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
-    choose_shapes(I, group_lanes, ctas_per_sm);
+    choose_shapes(I, group_lanes, lanes_used, ctas_per_sm);
     return MP_OK;
 }
 
@@ -718,14 +734,14 @@ namespace {
 cudaError_t prepare(mp_instance *I, bool argmin, long long max_rows) {
     cudaError_t e;
     if (!I->main.onchip) {
-        e = I->main_state.ensure(static_cast<size_t>(I->main.ctas) * I->main.groups_per_cta * I->main_so.bytes);
+        e = I->main_state.ensure(static_cast<size_t>(I->main.ctas) * (I->main.groups_per_cta + 1) * I->main_so.bytes);
         if (e != cudaSuccess) return e;
     }
     if ((e = I->ctrs.ensure(64)) != cudaSuccess) return e;
     const int nb = I->main.ctas + I->wide.ctas;
     if ((e = I->cta_best.ensure(static_cast<size_t>(nb) * 16 + 64)) != cudaSuccess) return e;
     if (I->main_rcap < I->ready_bound) {
-        e = I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes);
+        e = I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes);
         if (e != cudaSuccess) return e;
         e = I->ovf_rows.ensure(static_cast<size_t>(std::max(1LL, max_rows)) * 8);
         if (e != cudaSuccess) return e;
@@ -931,7 +947,7 @@ int32_t mp_enumerate_argmin(mp_instance *I, const int32_t *op_order, uint64_t fi
     const bool use_main = I->main_rcap >= I->ready_bound;
     MP_CUDA(prepare(I, true, 1));
     if (!use_main) {
-        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes));
+        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes));
     }
     const int nb = I->main.ctas + I->wide.ctas;
     k_init_best<<<std::max(1, (nb + 255) / 256), 256, 0, s>>>(best_ms_arr(I), best_row_arr(I), nb);
@@ -972,7 +988,7 @@ int32_t mp_schedule_one(mp_instance *I, const uint8_t *placement, double *starts
     MP_CUDA(cudaSetDevice(I->device));
     cudaStream_t s = I->stream;
     const int n = I->n_ops, N = I->n_nodes;
-    MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide_so.bytes)));
+    MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide_so.bytes) * 2));
     const size_t need = align16(n + 16) + 16ULL * N + 64 + 64;
     MP_CUDA(I->small.ensure(need));
     unsigned char *base = static_cast<unsigned char *>(I->small.p);
@@ -1007,6 +1023,7 @@ int32_t mp_schedule_one(mp_instance *I, const uint8_t *placement, double *starts
     one.threads = 32;
     one.groups_per_cta = 1;
     a.groups_per_cta = 1;
+    a.lanes_used = 32;
     MP_CUDA(mp_launch_eval(one, SRC_LOAD, true, a, s));
     double hms = 0;
     int8_t hst = 0;
@@ -1044,9 +1061,9 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     // an exact evaluation needs a ready capacity that covers the bound on-chip
     const bool onchip = I->main.onchip && I->main_rcap >= I->ready_bound;
     if (!I->main.onchip) {
-        MP_CUDA(I->main_state.ensure(static_cast<size_t>(I->main.ctas) * I->main.groups_per_cta * I->main_so.bytes));
+        MP_CUDA(I->main_state.ensure(static_cast<size_t>(I->main.ctas) * (I->main.groups_per_cta + 1) * I->main_so.bytes));
     } else if (!onchip) {
-        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * I->wide.groups_per_cta * I->wide_so.bytes));
+        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes));
     }
     const size_t seed_b = align16(static_cast<size_t>(n_seed) * n);
     const size_t rows_b = align16(static_cast<size_t>(n_chains) * n);

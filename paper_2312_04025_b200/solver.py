@@ -130,11 +130,12 @@ class Instance:
         self._lib.mp_instance_info_get(self._h, C.byref(inf))
         return {f: getattr(inf, f) for f, _ in N.mp_instance_info._fields_}
 
-    def tune(self, group_lanes: int = 0, ctas_per_sm: int = 0, ready_cap: int = 0, colo: bool = True) -> None:
+    def tune(self, group_lanes: int = 0, ctas_per_sm: int = 0, ready_cap: int = 0, colo: bool = True,
+             lanes_used: int = 0) -> None:
         """Launch-shape knobs (results never depend on them)."""
         flags = 0 if colo else 1
-        if self._lib.mp_instance_tune(self._h, group_lanes, ctas_per_sm, ready_cap, flags) != 0:
-            raise ValueError("group_lanes must be one of 0, 2, 4, 8, 16, 32")
+        if self._lib.mp_instance_tune(self._h, group_lanes, lanes_used, ctas_per_sm, ready_cap, flags) != 0:
+            raise ValueError("group_lanes in {0,1,2,4,8,16,32}; lanes_used a multiple of it, <= 32")
 
     # -- placement encoding -------------------------------------------------------
     def encode(self, assignments) -> np.ndarray:

@@ -27,7 +27,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--rows", type=int, default=1 << 18)
-    ap.add_argument("--G", default="4,8,16,32")
+    ap.add_argument("--G", default="1:8,1:16,1:32,2:16,2:32,4:32,8:32", help="G or G:U list")
+    ap.add_argument("--rcap", type=int, default=0)
+    ap.add_argument("--no-colo", action="store_true")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     args = ap.parse_args()
@@ -41,8 +43,9 @@ def main():
     st = torch.empty(args.rows, dtype=torch.int8, device="cuda")
     stream = torch.cuda.current_stream()
     lib = N.lib()
-    for G in [int(x) for x in args.G.split(",")]:
-        inst.tune(G, args.ctas_per_sm)
+    for spec in args.G.split(","):
+        G, U = (int(x) for x in (spec.split(":") + ["0"])[:2])
+        inst.tune(G, args.ctas_per_sm, ready_cap=args.rcap, colo=not args.no_colo, lanes_used=U)
         info = inst.info()
         best = C.c_int64()
         bms = C.c_double()
@@ -67,7 +70,7 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         t = min(times)
-        print(f"{w.name} G={G} warps/cta={info['groups_per_cta'] * G // 32} gpc={info['groups_per_cta']} "
+        print(f"{w.name} G={G} U={info['lanes_used']} colo={info['colo']} gpc={info['groups_per_cta']} "
               f"ctas={info['ctas']} rcap={info['ready_cap']} smem={info['smem_bytes']} state={info['state_bytes']} "
               f"tables={info['table_bytes']}: {args.rows / t:,.0f} placements/s ({t * 1e3:.2f} ms) best={best.value}",
               flush=True)

@@ -213,8 +213,9 @@ def random_problem(rng, n_ops, k, tight=False, ties=False, zero=False):
     return g, mp.Cluster([mp.Device(d, cap) for d in range(k)], links)
 
 
-SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (2, 4, 8, 16, 32) for colo in (True, False)
-          for rc in (0, 3)]
+SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (1, 2, 4, 8, 16, 32) for colo in (True, False)
+          for rc in (0, 3)] + [dict(group_lanes=1, lanes_used=8), dict(group_lanes=2, lanes_used=16),
+                               dict(group_lanes=4, lanes_used=8, ready_cap=2)]
 
 
 @pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
@@ -249,7 +250,7 @@ def test_eval_vs_oracle_workloads(oracle_mod, name):
         orc = oracle_mod.OracleInstance.from_instance(inst)
         rows = workloads.placements(w.seed, 4096 if name != "c5" else 256, inst.n_ops, inst.K)
         want, wst = orc.eval_batch(rows, threads=8)
-        for shape in (dict(), dict(group_lanes=8), dict(group_lanes=32, colo=False)):
+        for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False)):
             inst.tune(**shape)
             ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
             assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)
