@@ -1,0 +1,436 @@
+#!/usr/bin/env python3
+"""Headline benchmark: candidate placements evaluated per second (makespan).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[1]): the BERT-large inference graph (embed + 24
+encoder layers, 481 raw ops) coarsened by GCOF on the GPU to 265 ops / 360
+flows, placed on the Table-III intra-server cluster (V100, V100, P100, P100).
+A step evaluates one batch of ROWS random placements per GPU (uint8 device
+indices from PCG64(2 + 1000*rank): weak scaling, each rank a disjoint shard)
+and reduces the best placement across GPUs (16-byte NCCL all-gather of
+(makespan bits, global row)).  Inputs are 278 MB per GPU per step (> L2).
+
+value  = device-resident throughput: rows already in HBM, max time over ranks.
+e2e    = the same step through the C ABI with HOST (pinned) buffers: H2D of the
+         rows and D2H of every makespan inside the timed region.
+Reference arm (--impl reference): the reference algorithm in pure Python
+(oracle/pyref.py, faithful to opplace._schedule) on every host core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "candidate placements evaluated/sec (makespan) at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "placements/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---- workload (built identically on every rank) ------------------------------------------
+def build_workload(name: str):
+    from paper_2312_04025_b200 import workloads
+
+    return {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c2k8": lambda: workloads.c2(8),
+            "c3": workloads.c3, "c4": workloads.c4}[name]()
+
+
+def coarse_on_cpu(w):
+    """The coarse graph via the CPU oracle (reference arm only; identical to the
+    GPU gcof by tests/test_gpu_parity.py)."""
+    import paper_2312_04025_b200 as mp
+    from oracle.oracle import gcof_partition, materialize
+    from paper_2312_04025_b200.fusion import _Flat
+
+    k = _Flat(w.raw, w.rules, None).keep
+    nodes, edges = materialize(w.raw, gcof_partition(k[1], k[2], k[3], k[6], k[7], k[10], k[11]))
+    return mp.CompGraph([mp.OpNode(i, t, mem, cost, m, s, mp.Tag(tag)) for i, t, m, s, tag, mem, cost in nodes],
+                        [mp.FlowEdge(*e) for e in edges])
+
+
+def flat_arrays(g, cluster):
+    import paper_2312_04025_b200 as mp
+
+    mesh = mp.effective_bandwidth(cluster)
+    ids = g.node_ids
+    devs = cluster.device_ids
+    dg = g.csr()
+    K = len(devs)
+    bw = np.zeros((K, K))
+    for a, da in enumerate(devs):
+        for b, db in enumerate(devs):
+            if a != b:
+                bw[a, b] = mesh.bandwidth(da, db)
+    return (np.array([[g.node(i).compute_time[d] for d in devs] for i in ids], dtype=np.float64),
+            np.array([g.node(i).mem_bytes for i in ids], dtype=np.int64), dg.esrc, dg.edst, dg.payload,
+            np.array([cluster.device(d).mem_bytes for d in devs], dtype=np.int64), bw)
+
+
+# ---- CPU baselines ---------------------------------------------------------------------
+def cpu_baseline_python(arrays, rows_all, seconds: float):
+    """The reference algorithm in pure Python on every host core (bounded sample)."""
+    from oracle import pyref
+
+    inst = pyref.Instance.from_arrays(arrays)
+    t0 = time.perf_counter()
+    pyref.eval_rows(inst, rows_all[:20])
+    per_row = (time.perf_counter() - t0) / 20
+    cores = os.cpu_count() or 1
+    n = int(max(cores * 4, min(len(rows_all), seconds / per_row * cores)))
+    dt, _, procs = pyref.time_all_cores(arrays, rows_all[:n], processes=cores)
+    return {"value": n / dt, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"first {n} placements of the workload stream, pure-Python restatement of "
+                      f"opplace._schedule (oracle/pyref.py), {procs} processes, {dt:.1f} s"}
+
+
+def cpu_baseline_native(arrays, rows_all, seconds: float):
+    """The C restatement (oracle/moirai_oracle.c) on every host core — a far
+    stronger CPU baseline than the reference's own Python, reported alongside."""
+    from oracle.oracle import OracleInstance
+
+    orc = OracleInstance(*arrays)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    orc.eval_batch(rows_all[:2000], threads=cores)
+    per = (time.perf_counter() - t0) / 2000
+    n = int(min(len(rows_all), max(10000, seconds / per)))
+    t0 = time.perf_counter()
+    orc.eval_batch(rows_all[:n], threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {n} placements, C restatement (oracle/moirai_oracle.c), {cores} pthreads, {dt:.1f} s"}
+
+
+# ---- clocks ------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait(timeout=5)
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    p = ROOT / "profiles" / "ncu_eval_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+# ---- our arm -----------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_04025_b200 as mp
+    from paper_2312_04025_b200 import _native as N
+    from paper_2312_04025_b200 import workloads
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = build_workload(args.workload)
+    t0 = time.perf_counter()
+    coarse = mp.gcof(w.raw, w.rules, device=local)
+    t_gcof = time.perf_counter() - t0
+    inst = mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster), device=local)
+    if args.tune:
+        G, U, rc = (int(x) for x in (args.tune.split(":") + ["0", "0"])[:3])
+        inst.tune(G, 0, rc, True, U)
+    info = inst.info()
+    P = args.rows
+    n_ops = inst.n_ops
+    rows = workloads.placements(w.seed + 1000 * rank, P, n_ops, inst.K)
+    h_rows = torch.from_numpy(rows).pin_memory()
+    d_rows = h_rows.cuda()
+    d_ms = torch.empty(P, dtype=torch.float64, device="cuda")
+    d_st = torch.empty(P, dtype=torch.int8, device="cuda")
+    h_ms = torch.empty(P, dtype=torch.float64).pin_memory()
+    stream = torch.cuda.current_stream()
+    lib = N.lib()
+    err = N.mp_error()
+    best = C.c_int64()
+    bms = C.c_double()
+    gather_in = torch.zeros(2, dtype=torch.int64, device="cuda")
+    gather_out = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+
+    def exchange():
+        """Global keep-best: 16 B per rank over NCCL, lexicographic min on the host
+        (makespans are non-negative doubles, so their bits order like the values)."""
+        if best.value < 0:
+            mine = (np.float64(np.inf).view(np.int64), -1)
+        else:
+            mine = (np.float64(bms.value).view(np.int64), best.value + rank * P)
+        gather_in[0] = int(mine[0])
+        gather_in[1] = int(mine[1])
+        if world > 1:
+            dist.all_gather_into_tensor(gather_out, gather_in)
+            recs = gather_out.view(world, 2).cpu().numpy()
+        else:
+            recs = gather_in.view(1, 2).cpu().numpy()
+        recs = [(int(a), int(b)) for a, b in recs if b >= 0]
+        return min(recs) if recs else (None, -1)
+
+    def step_device():
+        code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(d_rows.data_ptr()), P, C.c_void_p(d_ms.data_ptr()),
+                                      C.c_void_p(d_st.data_ptr()), C.byref(best), C.byref(bms), N.MP_DEVICE_PTRS,
+                                      C.c_void_p(stream.cuda_stream), C.byref(err))
+        N.check(code, err, "mp_evaluate_argmin")
+        return exchange()
+
+    def step_host():
+        code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(h_rows.data_ptr()), P, C.c_void_p(h_ms.data_ptr()),
+                                      None, C.byref(best), C.byref(bms), 0, C.c_void_p(stream.cuda_stream),
+                                      C.byref(err))
+        N.check(code, err, "mp_evaluate_argmin(host)")
+        return exchange()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step_device()
+    # ---- timed region: device-resident -------------------------------------------------
+    clocks = ClockSampler(local) if rank == 0 else None
+    barrier()
+    launches0 = lib.mp_launch_count()
+    kern_ms = []
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    result = None
+    for _ in range(args.steps):
+        k0 = torch.cuda.Event(enable_timing=True)
+        k1 = torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(d_rows.data_ptr()), P, C.c_void_p(d_ms.data_ptr()),
+                                      C.c_void_p(d_st.data_ptr()), C.byref(best), C.byref(bms), N.MP_DEVICE_PTRS,
+                                      C.c_void_p(stream.cuda_stream), C.byref(err))
+        N.check(code, err)
+        k1.record(stream)
+        result = exchange()
+        kern_ms.append((k0, k1))
+    e_end.record(stream)
+    barrier()
+    launches = lib.mp_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    t_dev = max_over_ranks(e_start.elapsed_time(e_end) / 1e3)
+    t_kern = statistics.mean(a.elapsed_time(b) / 1e3 for a, b in kern_ms)
+    value = world * P * args.steps / t_dev
+
+    # ---- e2e: host buffers through the C ABI --------------------------------------------
+    for _ in range(max(1, args.warmup // 2)):
+        step_host()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_host()
+    barrier()
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    e2e = world * P * args.steps / t_e2e
+    assert np.array_equal(h_ms.numpy().view(np.uint64), d_ms.cpu().numpy().view(np.uint64)), "host/device mismatch"
+
+    # ---- local search throughput (secondary, untimed by the driver) ----------------------
+    ls = None
+    if args.local_search and rank == 0:
+        seeds = rows[:64]
+        t0 = time.perf_counter()
+        _, ls_best, _, _ = mp.local_search(inst, seeds, chains=8192, moves=32, seed=1)
+        dt = time.perf_counter() - t0
+        ls = {"chains": 8192, "moves": 32, "evals_per_s": 8192 * 33 / dt, "best_makespan_s": ls_best}
+
+    out = None
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        bytes_per = n_ops + 8  # one uint8 device id per op in, one fp64 makespan out (SURVEY §8(d) B_hbm)
+        achieved = P * bytes_per / t_kern / 1e9
+        tr = ncu_traffic()
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": (tr or {}).get("dram_bytes_per_launch"), "peak_source": peak_kind,
+                "algorithmic_bytes_per_placement": bytes_per, "kernel_ms": t_kern * 1e3,
+                "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan"}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name + f" (GCOF {len(w.raw)} -> {n_ops} ops / {inst.n_flows} flows, K={inst.K})",
+                       "rows_per_gpu": P, "global_rows_per_step": P * world, "parallelism": f"dp{world} (row shards)",
+                       "placements": "PCG64(seed=2+1000*rank) uint8 device indices",
+                       "l2": f"inputs larger than L2 ({P * n_ops / 1e6:.0f} MB per GPU per step)",
+                       "shape": {k: info[k] for k in ("group_lanes", "lanes_used", "groups_per_cta", "ctas",
+                                                       "ready_cap", "colo", "onchip", "smem_bytes")},
+                       "gcof_ms": t_gcof * 1e3},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": P * n_ops, "d2h_bytes_per_step": P * 8 + 16},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "clocks": clk,
+            "best": {"makespan_s": float(np.int64(result[0]).view(np.float64)) if result[1] >= 0 else None,
+                     "global_row": result[1]},
+        }
+        if ls:
+            out["local_search"] = ls
+        if world == 1 and not args.no_cpu:
+            arrays = inst._arrays
+            out["cpu_baseline"] = cpu_baseline_python(arrays, rows, args.cpu_seconds)
+            out["cpu_baseline_native"] = cpu_baseline_native(arrays, rows, args.cpu_seconds / 3)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    inst.close()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+# ---- reference arm -------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import pyref
+    from paper_2312_04025_b200 import workloads
+
+    w = build_workload(args.workload)
+    g = coarse_on_cpu(w)
+    arrays = flat_arrays(g, w.cluster)
+    n_ops = len(g)
+    K = len(w.cluster.device_ids)
+    cores = os.cpu_count() or 1
+    # size one step for ~args.ref_step_s seconds of all-core work
+    inst = pyref.Instance.from_arrays(arrays)
+    probe = workloads.placements(w.seed, 20, n_ops, K)
+    t0 = time.perf_counter()
+    pyref.eval_rows(inst, probe)
+    per_row = (time.perf_counter() - t0) / 20
+    n = int(max(cores * 2, args.ref_step_s / per_row * cores))
+    rows = workloads.placements(w.seed, n * (args.steps + args.warmup), n_ops, K)
+    import multiprocessing as mpc
+
+    procs = cores
+    ctx = mpc.get_context("fork")
+    with ctx.Pool(procs, initializer=pyref._worker_init, initargs=(arrays,)) as pool:
+        pool.map(pyref._worker_rows, [rows[i:i + 1] for i in range(procs)])
+        for s in range(args.warmup):
+            chunk = rows[s * n:(s + 1) * n]
+            pool.map(pyref._worker_rows, [chunk[i::procs] for i in range(procs)])
+        t0 = time.perf_counter()
+        for s in range(args.warmup, args.warmup + args.steps):
+            chunk = rows[s * n:(s + 1) * n]
+            pool.map(pyref._worker_rows, [chunk[i::procs] for i in range(procs)])
+        dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    sample = (f"{n} placements per step of the {w.name} stream (GCOF {len(w.raw)} -> {n_ops} ops), pure-Python "
+              f"restatement of opplace._schedule (oracle/pyref.py), {procs} processes")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": w.name + f" (GCOF {len(w.raw)} -> {n_ops} ops, K={K})", "rows_per_step": n,
+                      "parallelism": f"{procs} host processes"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="c2", choices=("c1", "c2", "c2k8", "c3", "c4"))
+    ap.add_argument("--rows", type=int, default=1 << 20, help="placements per GPU per step")
+    ap.add_argument("--tune", default="", help="G:U:ready_cap launch-shape override")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=2.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--local-search", action="store_true", default=True)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

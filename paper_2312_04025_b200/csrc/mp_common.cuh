@@ -89,6 +89,7 @@ struct EvalArgs {
     long long *ovf_rows;          // rows that overflowed the on-chip ready capacity
     unsigned int *ovf_count;
 
+    unsigned int *peak_ready;     // optional: atomicMax of the largest ready set seen (calibration)
     unsigned long long *next;     // work counter (rows handed out)
     unsigned char *gstate;        // global-state slots (off-chip mode)
     int groups_per_cta;

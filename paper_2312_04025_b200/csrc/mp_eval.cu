@@ -103,6 +103,7 @@ struct RowResult {
     double ms;
     int status;      // MP_ROW_* or MP_ROW_OVERFLOW
     int over_dev;
+    int peak;        // largest ready set during the dispatch
     long long over_by;
 };
 
@@ -144,6 +145,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     res.status = MP_ROW_OK;
     res.over_dev = -1;
     res.over_by = 0;
+    res.peak = 0;
 
     // ---- 1. memory feasibility (solver.py:82-87) ------------------------------
     double *clk = slot<double>(st, a.so.clk);
@@ -254,6 +256,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
 
     bool done = !alive || ovf;
     double ms = 0.0;
+    int peak = nready;
     while (__any_sync(kFull, !done)) {
         // -- local minimum over this lane's slice of the ready set (branch-free) ---
         const int maxr = __reduce_max_sync(kFull, done ? 0 : nready);
@@ -394,11 +397,13 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             }
             nready += __popc(bal & gbits);
         }
+        peak = (!done && nready > peak) ? nready : peak;
         const bool over = !done && nready > rcap;
         ovf = ovf || over;
         done = done || over || nready == 0;  // nready == 0: every node committed
         __syncwarp();
     }
+    res.peak = peak;
     if (!alive) return res;
     if (ovf) {
         res.status = MP_ROW_OVERFLOW;
@@ -513,6 +518,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __gri
         }
         __syncwarp();
         const RowResult r = eval_lockstep<G, TRACE, COLO>(a, tb, st, dev, gl, live);
+        if (live && gl == 0 && a.peak_ready) atomicMax(a.peak_ready, static_cast<unsigned int>(r.peak));
         if (live && gl == 0) {
             const long long o = grow - a.out_base;
             if (r.status == MP_ROW_OVERFLOW) {

@@ -306,6 +306,7 @@ struct mp_instance {
     bool colo = false;     // co-located flows skipped
     int sms = 0;
     int rcap_target = 32;
+    int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
     TabOff to{};
     unsigned char *blob = nullptr;
     // main (on-chip when possible) and off-chip variants
@@ -339,7 +340,9 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     // outgrows it are re-run by the off-chip variant with capacity = bound.
     int rcap = std::max(1, std::min(I->ready_bound, I->rcap_target));
     StOff so = make_stoff(n_ops, I->n_multi, K, rcap);
-    const int G = G_req > 0 ? G_req : (I->ready_bound <= 16 ? 4 : 8);
+    // lanes per placement from the typical ready-set size: a lane holds about one entry
+    const int typical = I->peak_probe > 0 ? I->peak_probe : I->ready_bound;
+    const int G = G_req > 0 ? G_req : (typical <= 8 ? 4 : (typical <= 32 ? 8 : (typical <= 96 ? 16 : 32)));
     // slots that fit next to the tables (one extra dummy slot for idle lanes)
     const long long avail = static_cast<long long>(smem_cap) - I->to.bytes;
     const long long slots = avail > 0 ? avail / so.bytes - 1 : 0;
@@ -664,6 +667,44 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     }
 
     choose_shapes(I, 0, 0, 0);
+    // Calibration probe: evaluate a few random placements with the exact off-chip
+    // variant and size the on-chip ready capacity from the largest ready set seen
+    // (x2 headroom).  Rows that still outgrow it are re-run off-chip, so results
+    // never depend on this choice — only speed does.
+    {
+        const int P = 128;
+        std::vector<uint8_t> rows(static_cast<size_t>(P) * n_ops);
+        unsigned long long x = 0x9e3779b97f4a7c15ULL;
+        for (auto &v : rows) {
+            x ^= x << 13;
+            x ^= x >> 7;
+            x ^= x << 17;
+            v = static_cast<uint8_t>(x % static_cast<unsigned long long>(K));
+        }
+        DevBuf pb;
+        MP_CUDA_I(pb.ensure(rows.size() + 64));
+        MP_CUDA_I(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes));
+        MP_CUDA_I(I->ctrs.ensure(64));
+        MP_CUDA_I(I->ovf_rows.ensure(64));
+        unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
+        MP_CUDA_I(cudaMemsetAsync(ctr, 0, 64, I->stream));
+        MP_CUDA_I(cudaMemcpyAsync(pb.p, rows.data(), rows.size(), cudaMemcpyHostToDevice, I->stream));
+        EvalArgs a = base_args(I, true);
+        a.rows = static_cast<const uint8_t *>(pb.p);
+        a.n_rows = P;
+        a.rows_bytes = static_cast<long long>(rows.size());
+        a.next = ctr;
+        a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
+        a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+        a.peak_ready = reinterpret_cast<unsigned int *>(ctr + 4);
+        MP_CUDA_I(mp_launch_eval(I->wide, SRC_LOAD, false, a, I->stream));
+        unsigned int peak = 0;
+        MP_CUDA_I(cudaMemcpyAsync(&peak, ctr + 4, 4, cudaMemcpyDeviceToHost, I->stream));
+        MP_CUDA_I(cudaStreamSynchronize(I->stream));
+        I->peak_probe = static_cast<int>(peak);
+        I->rcap_target = std::max(4, 2 * static_cast<int>(peak));
+        choose_shapes(I, 0, 0, 0);
+    }
     *out = I;
     return MP_OK;
 #undef MP_CUDA_I
@@ -703,6 +744,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->ready_bound = I->ready_bound;
     info->colo = I->colo ? 1 : 0;
     info->colo_ok = I->colo_ok ? 1 : 0;
+    info->peak_probe = I->peak_probe;
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
     return MP_OK;
@@ -719,7 +761,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
         return MP_ERR_INVALID;
     if (ready_cap < 0 || ctas_per_sm < 0) return MP_ERR_INVALID;
     std::lock_guard<std::mutex> lk(I->mu);
-    I->rcap_target = ready_cap > 0 ? ready_cap : 32;
+    I->rcap_target = ready_cap > 0 ? ready_cap : (I->peak_probe > 0 ? std::max(4, 2 * I->peak_probe) : 32);
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm);
     return MP_OK;
