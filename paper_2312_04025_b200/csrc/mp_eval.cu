@@ -471,7 +471,7 @@ __device__ __forceinline__ int group_of_lane(const EvalArgs &a, int lane, bool &
 
 // ---- K3/K4: batch evaluation with fused keep-best ---------------------------------
 template <int G, int SRC, bool ONCHIP, bool TRACE, bool COLO>
-__global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
+__global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 32];
@@ -555,10 +555,13 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 // Chain c: start from seed row c % n_seed, then `moves` proposals: move t
 // re-assigns op (h % n_ops) to a different device drawn from h >> 32, where
 // h = mix64(rng_seed ^ mix64(c * PHI + t)).  Accept iff the makespan does not
-// increase.  Proposals depend only on (rng_seed, c, t): results are identical
-// for any G, grid or GPU count.
+// increase.  Proposals depend only on (rng_seed, c, t).  A proposal whose
+// evaluation outgrows the on-chip ready capacity (rare by construction of the
+// capacity) counts as rejected; every makespan a chain carries is
+// an exact evaluation.  Results are identical for any G or GPU count at a fixed
+// ready capacity.
 template <int G, bool ONCHIP, bool COLO>
-__global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_ls_kernel(const __grid_constant__ EvalArgs a,
+__global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                      const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
@@ -599,7 +602,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS) mp_ls_kernel(const __grid_
             const RowResult r = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live);
             const double ms = r.status == MP_ROW_OK ? r.ms : kInf;
             __syncwarp();
-            if (ms <= cur_ms) {
+            if (r.status != MP_ROW_OVERFLOW && ms <= cur_ms) {
                 cur_ms = ms;
             } else if (live && gl == 0) {
                 dev[i] = static_cast<unsigned char>(old);

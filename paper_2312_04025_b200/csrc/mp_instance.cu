@@ -1100,12 +1100,10 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     const int n = I->n_ops;
     for (long long r = 0; r < static_cast<long long>(n_seed) * n; ++r)
         if (seed_rows[r] >= I->K) return set_err(err, MP_ERR_BAD_DEVICE, r / n, seed_rows[r], "seed row names an unknown device");
-    // an exact evaluation needs a ready capacity that covers the bound on-chip
-    const bool onchip = I->main.onchip && I->main_rcap >= I->ready_bound;
+    // The main shape runs the chains; a proposal that overflows its on-chip
+    // ready capacity is rejected (mp_ls_kernel), so every kept makespan is exact.
     if (!I->main.onchip) {
         MP_CUDA(I->main_state.ensure(static_cast<size_t>(I->main.ctas) * (I->main.groups_per_cta + 1) * I->main_so.bytes));
-    } else if (!onchip) {
-        MP_CUDA(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes));
     }
     const size_t seed_b = align16(static_cast<size_t>(n_seed) * n);
     const size_t rows_b = align16(static_cast<size_t>(n_chains) * n);
@@ -1122,7 +1120,7 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     MP_CUDA(I->ovf_rows.ensure(64));
     unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
     MP_CUDA(cudaMemsetAsync(ctr, 0, 64, s));
-    const bool use_wide = I->main.onchip && !onchip;
+    const bool use_wide = false;
     EvalArgs a = base_args(I, use_wide);
     a.next = ctr;
     a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
