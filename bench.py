@@ -226,22 +226,17 @@ def run_ours(args):
     gather_in = torch.zeros(2, dtype=torch.int64, device="cuda")
     gather_out = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
 
+    from paper_2312_04025_b200.distributed import combine_records, encode_record
+
     def exchange():
-        """Global keep-best: 16 B per rank over NCCL, lexicographic min on the host
-        (makespans are non-negative doubles, so their bits order like the values)."""
-        if best.value < 0:
-            mine = (np.float64(np.inf).view(np.int64), -1)
-        else:
-            mine = (np.float64(bms.value).view(np.int64), best.value + rank * P)
-        gather_in[0] = int(mine[0])
-        gather_in[1] = int(mine[1])
+        """Global keep-best: a 16-byte (makespan bits, global row) record per rank,
+        all-gathered over NCCL, lexicographic minimum (paper_2312_04025_b200.distributed)."""
+        rec = encode_record(bms.value, best.value + rank * P if best.value >= 0 else -1)
+        gather_in.copy_(torch.from_numpy(rec), non_blocking=True)
         if world > 1:
             dist.all_gather_into_tensor(gather_out, gather_in)
-            recs = gather_out.view(world, 2).cpu().numpy()
-        else:
-            recs = gather_in.view(1, 2).cpu().numpy()
-        recs = [(int(a), int(b)) for a, b in recs if b >= 0]
-        return min(recs) if recs else (None, -1)
+            return combine_records(gather_out.cpu().numpy())
+        return combine_records(gather_in.cpu().numpy())
 
     def step_device():
         code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(d_rows.data_ptr()), P, C.c_void_p(d_ms.data_ptr()),
@@ -327,7 +322,8 @@ def run_ours(args):
         achieved = P * bytes_per / t_kern / 1e9
         tr = ncu_traffic()
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": (tr or {}).get("dram_bytes_per_launch"), "peak_source": peak_kind,
+                "traffic": (tr["dram_bytes_per_row"] * P if tr and "dram_bytes_per_row" in tr else None),
+                "traffic_source": (tr or {}).get("source"), "peak_source": peak_kind,
                 "algorithmic_bytes_per_placement": bytes_per, "kernel_ms": t_kern * 1e3,
                 "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan"}
         out = {
@@ -345,8 +341,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": roof,
             "clocks": clk,
-            "best": {"makespan_s": float(np.int64(result[0]).view(np.float64)) if result[1] >= 0 else None,
-                     "global_row": result[1]},
+            "best": {"makespan_s": result[0] if result[1] >= 0 else None, "global_row": result[1]},
         }
         if ls:
             out["local_search"] = ls
