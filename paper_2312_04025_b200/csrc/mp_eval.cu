@@ -99,6 +99,10 @@ __device__ __forceinline__ bool key_less_nb(unsigned long long e, unsigned long 
     return elt | (eeq & (rgt | (req & nlt)));
 }
 
+__device__ __forceinline__ double4 make_entry(double est, double rank, double dur, uint32_t meta, uint32_t tie) {
+    return make_double4(est, rank, dur, bitsd((static_cast<unsigned long long>(tie) << 32) | meta));
+}
+
 struct RowResult {
     double ms;
     int status;      // MP_ROW_* or MP_ROW_OVERFLOW
@@ -220,11 +224,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     double *m_est = slot<double>(st, a.so.m_est);
     uint32_t *m_tie = slot<uint32_t>(st, a.so.m_tie);
     uint16_t *m_np = slot<uint16_t>(st, a.so.m_np);
-    double *r_est = slot<double>(st, a.so.r_est);
-    double *r_rank = slot<double>(st, a.so.r_rank);
-    double *r_dur = slot<double>(st, a.so.r_dur);
-    uint32_t *r_meta = slot<uint32_t>(st, a.so.r_meta);
-    uint32_t *r_tie = slot<uint32_t>(st, a.so.r_tie);
+    // ready entries: 32-byte records {est, rank | dur, meta, tie}, read and
+    // written as two 16-byte vectors
+    double4 *rdy = slot<double4>(st, a.so.r_est);
     for (int k = gl; k < a.n_multi; k += G) {
         m_np[k] = static_cast<uint16_t>(tab<uint32_t>(tb, a.to.m_deg)[k]);
         m_est[k] = 0.0;
@@ -232,11 +234,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     }
     for (int k = gl; k <= static_cast<int>(WS); k += G) clk[k] = 0.0;
     if (gl == 0) {  // the branch-free scan may read entry 0 of an empty ready set
-        r_meta[0] = (RZ << 20) | (RZ << 26);
-        r_est[0] = 0.0;
-        r_rank[0] = 0.0;
-        r_dur[0] = 0.0;
-        r_tie[0] = 0;
+        rdy[0] = make_entry(0.0, 0.0, 0.0, (RZ << 20) | (RZ << 26), 0u);
     }
     __syncwarp();
     int nready = a.n_src;
@@ -245,11 +243,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         for (int t = gl; t < nready; t += G) {
             const int i = static_cast<int>(tab<uint32_t>(tb, a.to.srcs)[t]);
             const int d = dev[i];
-            r_est[t] = 0.0;
-            r_rank[t] = rank[i];
-            r_dur[t] = T_cost[i * K + d];
-            r_meta[t] = static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26);
-            r_tie[t] = static_cast<uint32_t>(i);
+            rdy[t] = make_entry(0.0, rank[i], T_cost[i * K + d],
+                                static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26),
+                                static_cast<uint32_t>(i));
         }
     }
     __syncwarp();
@@ -268,16 +264,19 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int s = s0 + gl;
             const bool valid = !done && s < nready;
             const int sc = valid ? s : 0;  // slot arrays always hold >= 1 entry
-            const uint32_t m = r_meta[sc];
-            const unsigned long long es = dbits(r_est[sc]);
+            const double2 h0 = reinterpret_cast<const double2 *>(rdy + sc)[0];
+            const double2 h1 = reinterpret_cast<const double2 *>(rdy + sc)[1];
+            const uint32_t m = static_cast<uint32_t>(dbits(h1.y));
+            const uint32_t tie = static_cast<uint32_t>(dbits(h1.y) >> 32);
+            const unsigned long long es = dbits(h0.x);
             const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
             const unsigned long long c1 = dbits(clk[i1 <= WS ? i1 : RZ]);
             const unsigned long long c2 = dbits(clk[i2 <= WS ? i2 : RZ]);
             unsigned long long e = es > c1 ? es : c1;
             e = e > c2 ? e : c2;
-            const unsigned long long r = dbits(r_rank[sc]);
-            const uint32_t id = (COLO && e == es) ? r_tie[sc] : (m & MP_NODE_MASK);
-            const double du = r_dur[sc];
+            const unsigned long long r = dbits(h0.y);
+            const uint32_t id = (COLO && e == es) ? tie : (m & MP_NODE_MASK);
+            const double du = h1.x;
             const bool take = valid & key_less_nb(e, r, id, be, br, bi);
             be = take ? e : be;
             br = take ? r : br;
@@ -287,9 +286,12 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             bs = take ? s : bs;
         }
         const uint32_t mine = bi;
-        // -- G-lane butterfly: every lane ends with its group's minimum -----------
+        // -- G-lane butterfly: every lane ends with its group's minimum.  Entries
+        //    sit on lanes 0..maxr-1 of each group, so rounds with o >= maxr only
+        //    exchange empty keys and are skipped (maxr is warp-uniform). --------
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) {
+            if (o >= maxr) continue;
             const unsigned long long e2 = __shfl_xor_sync(kFull, be, o, G);
             const unsigned long long r2 = __shfl_xor_sync(kFull, br, o, G);
             const uint32_t i2 = __shfl_xor_sync(kFull, bi, o, G);
@@ -304,13 +306,13 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         const int src_lane = own ? (__ffs(own) - 1) : lane;
         const uint32_t wmeta = __shfl_sync(kFull, bmeta, src_lane);
         const double wdur = __shfl_sync(kFull, bdur, src_lane);
+        be = __shfl_sync(kFull, be, src_lane);  // lanes >= maxr skipped butterfly rounds
         const int last = nready - 1;
         if (owner && bs != last) {  // unordered removal: move the last entry into the hole
-            r_est[bs] = r_est[last];
-            r_rank[bs] = r_rank[last];
-            r_dur[bs] = r_dur[last];
-            r_meta[bs] = r_meta[last];
-            r_tie[bs] = r_tie[last];
+            const double2 l0 = reinterpret_cast<const double2 *>(rdy + last)[0];
+            const double2 l1 = reinterpret_cast<const double2 *>(rdy + last)[1];
+            reinterpret_cast<double2 *>(rdy + bs)[0] = l0;
+            reinterpret_cast<double2 *>(rdy + bs)[1] = l1;
         }
         __syncwarp();
         nready = done ? nready : last;
@@ -383,11 +385,10 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const unsigned bal = __ballot_sync(kFull, ins);
             const int pos = nready + __popc(bal & below);
             if (ins && pos < rcap) {
-                r_est[pos] = flow_ins ? end : ej;
-                r_rank[pos] = flow_ins ? fdur + rj : rj;
-                r_dur[pos] = flow_ins ? fdur : odur;
-                r_meta[pos] = flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26));
-                r_tie[pos] = flow_ins ? pid : tie_j;
+                rdy[pos] = make_entry(flow_ins ? end : ej, flow_ins ? fdur + rj : rj, flow_ins ? fdur : odur,
+                                      flow_ins ? fmeta
+                                               : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                                      flow_ins ? pid : tie_j);
             }
             if constexpr (TRACE) {
                 if (act && via_colo) {  // zero-duration flow: start = end = producer's end

@@ -239,11 +239,8 @@ StOff make_stoff(int n_ops, int n_multi, int K, int rcap) {
     s.rank = take(8ULL * n_ops);
     s.m_est = take(8ULL * n_multi);
     s.clk = take(8ULL * (3 * K + 2));
-    s.r_est = take(8ULL * rcap);
-    s.r_rank = take(8ULL * rcap);
-    s.r_dur = take(8ULL * rcap);
-    s.r_meta = take(4ULL * rcap);
-    s.r_tie = take(4ULL * rcap);
+    s.r_est = take(32ULL * rcap);  // 32-byte AoS ready entries (mp_eval.cu make_entry)
+    s.r_rank = s.r_dur = s.r_meta = s.r_tie = s.r_est;
     s.m_tie = take(4ULL * n_multi);
     s.m_np = take(2ULL * n_multi);
     s.dev = take(static_cast<uint64_t>(n_ops) + 32);
