@@ -99,6 +99,8 @@ typedef struct mp_instance_info {
     int32_t colo;               /* 1: co-located flows are not dispatched (exact: all durations > 0) */
     int32_t colo_ok;            /* 1: the instance qualifies for colo                */
     int32_t peak_probe;         /* largest ready set on the creation-time calibration probe */
+    int32_t prefilter;          /* 1: a memory-feasibility pass compacts rows before scheduling */
+    int32_t mode;               /* 2: tables+state in smem, 1: state in smem, 0: all global */
     int64_t table_bytes;        /* instance tables staged per CTA                    */
     int64_t state_bytes;        /* per-placement dynamic state                       */
 } mp_instance_info;

@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "mp_common.cuh"
@@ -211,10 +212,10 @@ __device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, co
     return n;
 }
 
-// The reference DFS (fusion.py:281-303), replayed exactly by one thread.
-__global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
-                      int *stack, int *buf) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The reference DFS (fusion.py:281-303), replayed exactly by one thread over
+// the state `s` (shared or global memory, see k_dfs_smem).
+__device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, const Trie &t,
+                        const DfsState &s, int *stack, int *buf) {
     int two[2];
     for (int src = 0; src < V; ++src) {
         if (indeg[src] != 0) continue;  // sources of the input graph, ascending id
@@ -284,6 +285,85 @@ __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const 
                 if (!s.visited[buf[z]]) stack[sp++] = buf[z];
         }
     }
+}
+
+__global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
+                      int *stack, int *buf) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    dfs_run(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
+}
+
+// Small graphs: the whole DFS state, CSR and trie move into shared memory (one
+// CTA), the DFS runs on thread 0 at shared-memory latency, and the state is
+// written back for the parallel final partition.
+__global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int TN, const int *indeg, const int *obeg,
+                                                   const int *odst, Trie tg, DfsState sg, int stack_cap) {
+    extern __shared__ __align__(16) int smi[];
+    int *p = smi;
+    auto take = [&](int n) {
+        int *r = p;
+        p += (n + 3) & ~3;
+        return r;
+    };
+    DfsState s;
+    s.where = take(V);
+    s.next = take(V);
+    s.head = take(V);
+    s.tail = take(V);
+    s.state = take(V);
+    s.len = take(V);
+    s.tag = take(V);
+    s.seq = take(V * Lmax);
+    int *ind = take(V);
+    int *ob = take(V + 1);
+    int *od = take(E);
+    Trie t;
+    t.child = take(TN);
+    t.sibling = take(TN);
+    t.type = take(TN);
+    t.flags = take(TN);
+    int *stack = take(stack_cap);
+    int *buf = take(stack_cap);
+    s.visited = reinterpret_cast<unsigned char *>(p);
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        s.where[i] = sg.where[i];
+        s.next[i] = sg.next[i];
+        s.head[i] = sg.head[i];
+        s.tail[i] = sg.tail[i];
+        s.state[i] = sg.state[i];
+        s.len[i] = sg.len[i];
+        s.tag[i] = sg.tag[i];
+        s.visited[i] = 0;
+        ind[i] = indeg[i];
+    }
+    for (int i = threadIdx.x; i < V * Lmax; i += blockDim.x) s.seq[i] = sg.seq[i];
+    for (int i = threadIdx.x; i <= V; i += blockDim.x) ob[i] = obeg[i];
+    for (int i = threadIdx.x; i < E; i += blockDim.x) od[i] = odst[i];
+    for (int i = threadIdx.x; i < TN; i += blockDim.x) {
+        t.child[i] = tg.child[i];
+        t.sibling[i] = tg.sibling[i];
+        t.type[i] = tg.type[i];
+        t.flags[i] = tg.flags[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) dfs_run(V, Lmax, ind, ob, od, t, s, stack, buf);
+    __syncthreads();
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        sg.where[i] = s.where[i];
+        sg.next[i] = s.next[i];
+        sg.head[i] = s.head[i];
+        sg.tail[i] = s.tail[i];
+        sg.state[i] = s.state[i];
+        sg.len[i] = s.len[i];
+        sg.tag[i] = s.tag[i];
+    }
+    for (int i = threadIdx.x; i < V * Lmax; i += blockDim.x) sg.seq[i] = s.seq[i];
+}
+
+size_t dfs_smem_bytes(int V, int E, int Lmax, int TN, int stack_cap) {
+    auto r4 = [](size_t n) { return (n + 3) & ~size_t(3); };
+    return 4 * (7 * r4(V) + r4(static_cast<size_t>(V) * Lmax) + r4(V) + r4(V + 1) + r4(E) + 4 * r4(TN) +
+                2 * r4(stack_cap)) + static_cast<size_t>(V) + 16;
 }
 
 // final_partition (fusion.py:195-219): one thread per surviving group.
@@ -459,7 +539,8 @@ __global__ void k_edge_keys(int E, const int *src, const int *dst, const int *gr
     }
 }
 
-__global__ void k_edge_split(int n, const unsigned long long *keys, int *u, int *v) {
+__global__ void k_edge_split(const int *n_dev, const unsigned long long *keys, int *u, int *v) {
+    const int n = *n_dev;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         u[e] = static_cast<int>(keys[e] >> 32);
         v[e] = static_cast<int>(keys[e] & 0xffffffffULL);
@@ -477,6 +558,25 @@ struct Arena {
     }
 };
 
+// Per-device state kept across calls: stream, device arena, pinned staging.
+struct CoarsenCtx {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    unsigned char *dev = nullptr;
+    size_t dev_cap = 0;
+    unsigned char *pin = nullptr;
+    size_t pin_cap = 0;
+    bool smem_attr = false;
+};
+CoarsenCtx g_ctx[64];
+
+template <typename T>
+size_t put(unsigned char *pin, size_t off, const T *src, size_t n) {
+    const size_t at = (off + 255) & ~size_t(255);
+    if (n) memcpy(pin + at, src, n * sizeof(T));
+    return at;
+}
+
 }  // namespace
 
 extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coarsen_output *out, mp_error *err) {
@@ -487,7 +587,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     if (V < 0 || E < 0 || D < 1 || R < 0 || O < 0) return cset_err(err, MP_ERR_INVALID, V, E, "bad sizes");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return cset_err(err, MP_ERR_NO_GPU, 0, 0, "no CUDA device");
-    CK(cudaSetDevice(device));
+    if (device < 0 || device >= ndev || device >= 64) return cset_err(err, MP_ERR_INVALID, device, ndev, "bad device");
     if (V == 0) return MP_OK;
     const int S = in->seq_beg[V];
     const int RT = R ? in->rule_beg[R] : 0;
@@ -498,92 +598,115 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     for (int e = 0; e < E; ++e)
         if (in->esrc[e] < 0 || in->esrc[e] >= V || in->edst[e] < 0 || in->edst[e] >= V)
             return cset_err(err, MP_ERR_INVALID, e, 0, "edge %d has a bad endpoint", e);
-
-    cudaStream_t st;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    // ---- upload ------------------------------------------------------------------
+    CoarsenCtx &cx = g_ctx[device];
+    std::lock_guard<std::mutex> lk(cx.mu);
+    CK(cudaSetDevice(device));
+    if (!cx.st) CK(cudaStreamCreateWithFlags(&cx.st, cudaStreamNonBlocking));
+    cudaStream_t st = cx.st;
     const int TN = R * Lmax + 2;
-    // generous upper bound of every arena allocation below (each is 256-aligned)
-    size_t bytes = 96 * 512;
-    bytes += 4ULL * ((V + 1ULL) * 40 + 8ULL * E + S + RT + OT + 2ULL * O + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
-    bytes += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
-    size_t tmp_bytes = 0, t2 = 0, t3 = 0;
+
+    // ---- one packed upload through pinned staging ---------------------------------
+    size_t up_bytes = 0;
+    {
+        const size_t parts[] = {4ULL * (V + 1), 4ULL * S, 4ULL * V, 8ULL * V, 8ULL * V * D, 4ULL * E, 4ULL * E,
+                                8ULL * E, 4ULL * (R + 1), 4ULL * RT, 4ULL * (O + 1), 4ULL * OT, 4ULL * O, 8ULL * O};
+        for (size_t p : parts) up_bytes += ((p + 255) & ~size_t(255)) + 256;
+    }
+    const size_t down_bytes = 4ULL * 5 * (V + 8) + 8ULL * V + 8ULL * V * D + 4ULL * 2 * (E + 8) + 16ULL * (E + 8) + 4096;
+    const size_t pin_need = std::max(up_bytes, down_bytes);
+    if (cx.pin_cap < pin_need) {
+        if (cx.pin) cudaFreeHost(cx.pin);
+        cx.pin = nullptr;
+        cx.pin_cap = 0;
+        CK(cudaMallocHost(&cx.pin, pin_need));
+        cx.pin_cap = pin_need;
+    }
+    unsigned char *pin = cx.pin;
+    size_t o = 0;
+    const size_t u_seq_beg = put(pin, o, in->seq_beg, V + 1); o = u_seq_beg + 4ULL * (V + 1);
+    const size_t u_seq = put(pin, o, in->seq_types, S); o = u_seq + 4ULL * S;
+    const size_t u_tag = put(pin, o, in->tag, V); o = u_tag + 4ULL * V;
+    const size_t u_mem = put(pin, o, in->mem, V); o = u_mem + 8ULL * V;
+    const size_t u_cost = put(pin, o, in->cost, static_cast<size_t>(V) * D); o = u_cost + 8ULL * V * D;
+    const size_t u_esrc = put(pin, o, in->esrc, E); o = u_esrc + 4ULL * E;
+    const size_t u_edst = put(pin, o, in->edst, E); o = u_edst + 4ULL * E;
+    const size_t u_pay = put(pin, o, in->payload, E); o = u_pay + 8ULL * E;
+    const size_t u_rbeg = put(pin, o, R ? in->rule_beg : in->seq_beg, R ? R + 1 : 0); o = u_rbeg + 4ULL * (R + 1);
+    const size_t u_rt = put(pin, o, in->rule_types, RT); o = u_rt + 4ULL * RT;
+    const size_t u_obeg = put(pin, o, O ? in->ov_beg : in->seq_beg, O ? O + 1 : 0); o = u_obeg + 4ULL * (O + 1);
+    const size_t u_ot = put(pin, o, in->ov_types, OT); o = u_ot + 4ULL * OT;
+    const size_t u_odev = put(pin, o, in->ov_dev, O); o = u_odev + 4ULL * O;
+    const size_t u_otime = put(pin, o, in->ov_time, O); o = u_otime + 8ULL * O;
+    const size_t up_used = (o + 255) & ~size_t(255);
+
+    // ---- device arena ----------------------------------------------------------------
+    size_t tmp_bytes = 0, t2 = 0, t3 = 0, t4 = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (const unsigned long long *)nullptr,
                                    (unsigned long long *)nullptr, std::max(E, 1));
     cub::DeviceRadixSort::SortPairs(nullptr, t2, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                     (const long long *)nullptr, (long long *)nullptr, std::max(E, 1));
     cub::DeviceScan::ExclusiveSum(nullptr, t3, (const int *)nullptr, (int *)nullptr, V + 1);
-    size_t t4 = 0;
     cub::DeviceReduce::ReduceByKey(nullptr, t4, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                    (const long long *)nullptr, (long long *)nullptr, (int *)nullptr, cub::Sum(),
                                    std::max(E, 1));
     const size_t tmpb = std::max(std::max(tmp_bytes, t2), std::max(t3, t4)) + 256;
-    bytes += tmpb;
+    size_t need = up_used + tmpb + 96 * 512;
+    need += 4ULL * ((V + 1ULL) * 40 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
+    need += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
+    if (cx.dev_cap < need) {
+        if (cx.dev) cudaFree(cx.dev);
+        cx.dev = nullptr;
+        cx.dev_cap = 0;
+        CK(cudaMalloc(&cx.dev, need));
+        cx.dev_cap = need;
+    }
     Arena ar;
-    CK(cudaMalloc(&ar.base, bytes));
-    ar.cap = bytes;
-    auto up = [&](auto *dst, const auto *src, size_t n) -> cudaError_t {
-        if (n == 0) return cudaSuccess;
-        return cudaMemcpyAsync(dst, src, n * sizeof(*src), cudaMemcpyHostToDevice, st);
-    };
-    int *d_seq_beg = ar.take<int>(V + 1), *d_seq = ar.take<int>(S), *d_tag = ar.take<int>(V);
-    long long *d_mem = ar.take<long long>(V);
-    double *d_cost = ar.take<double>(static_cast<size_t>(V) * D);
-    int *d_esrc = ar.take<int>(E), *d_edst = ar.take<int>(E);
-    long long *d_pay = ar.take<long long>(E);
-    int *d_rbeg = ar.take<int>(R + 1), *d_rt = ar.take<int>(RT);
-    int *d_obeg = ar.take<int>(O + 1), *d_ot = ar.take<int>(OT), *d_odev = ar.take<int>(O);
-    double *d_otime = ar.take<double>(O);
-    int rc = MP_OK;
-    CK(up(d_seq_beg, in->seq_beg, V + 1));
-    CK(up(d_seq, in->seq_types, S));
-    CK(up(d_tag, in->tag, V));
-    CK(up(d_mem, reinterpret_cast<const long long *>(in->mem), V));
-    CK(up(d_cost, in->cost, static_cast<size_t>(V) * D));
-    CK(up(d_esrc, in->esrc, E));
-    CK(up(d_edst, in->edst, E));
-    CK(up(d_pay, reinterpret_cast<const long long *>(in->payload), E));
-    if (R) {
-        CK(up(d_rbeg, in->rule_beg, R + 1));
-        CK(up(d_rt, in->rule_types, RT));
-    }
-    if (O) {
-        CK(up(d_obeg, in->ov_beg, O + 1));
-        CK(up(d_ot, in->ov_types, OT));
-        CK(up(d_odev, in->ov_dev, O));
-        CK(up(d_otime, in->ov_time, O));
-    }
+    ar.base = cx.dev;
+    ar.cap = cx.dev_cap;
+    unsigned char *upd = ar.take<unsigned char>(up_used);
+    CK(cudaMemcpyAsync(upd, pin, up_used, cudaMemcpyHostToDevice, st));
+    const int *d_seq_beg = reinterpret_cast<const int *>(upd + u_seq_beg);
+    const int *d_seq = reinterpret_cast<const int *>(upd + u_seq);
+    const int *d_tag = reinterpret_cast<const int *>(upd + u_tag);
+    const long long *d_mem = reinterpret_cast<const long long *>(upd + u_mem);
+    const double *d_cost = reinterpret_cast<const double *>(upd + u_cost);
+    const int *d_esrc = reinterpret_cast<const int *>(upd + u_esrc);
+    const int *d_edst = reinterpret_cast<const int *>(upd + u_edst);
+    const long long *d_pay = reinterpret_cast<const long long *>(upd + u_pay);
+    const int *d_rbeg = reinterpret_cast<const int *>(upd + u_rbeg);
+    const int *d_rt = reinterpret_cast<const int *>(upd + u_rt);
+    const int *d_obeg = reinterpret_cast<const int *>(upd + u_obeg);
+    const int *d_ot = reinterpret_cast<const int *>(upd + u_ot);
+    const int *d_odev = reinterpret_cast<const int *>(upd + u_odev);
+    const double *d_otime = reinterpret_cast<const double *>(upd + u_otime);
     const int grid = std::max(1, std::min(2048, (std::max(V, E) + 255) / 256));
-    // ---- K1a: CSR sorted by (src, dst), degrees, cycle check ------------------------
+
+    // ---- K1a: CSR sorted by (src, dst), degrees, cycle check (read at the end) ----
     unsigned long long *keys = ar.take<unsigned long long>(E), *skeys = ar.take<unsigned long long>(E);
     int *indeg = ar.take<int>(V + 1), *outcnt = ar.take<int>(V + 1), *obeg = ar.take<int>(V + 1);
     int *odst = ar.take<int>(E);
-    int *deg = ar.take<int>(V + 1), *fa = ar.take<int>(V + 1), *fb = ar.take<int>(V + 1), *seen = ar.take<int>(4);
+    int *deg = ar.take<int>(V + 1), *fa = ar.take<int>(V + 1), *fb = ar.take<int>(V + 1);
+    int *counters = ar.take<int>(16);  // [0] kahn seen, [1] unique quotient edges
     void *tmp = ar.take<unsigned char>(tmpb);
     CK(cudaMemsetAsync(indeg, 0, 4ULL * (V + 1), st));
     CK(cudaMemsetAsync(outcnt, 0, 4ULL * (V + 1), st));
+    CK(cudaMemsetAsync(counters, 0, 64, st));
+    size_t tb;
     if (E) {
         k_make_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, keys, indeg);
         ++g_mp_launches;
-        size_t tb = tmpb;
+        tb = tmpb;
         CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, skeys, E, 0, 64, st));
         k_split_keys<<<grid, 256, 0, st>>>(E, skeys, odst, outcnt);
         ++g_mp_launches;
     }
-    {
-        size_t tb = tmpb;
-        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, outcnt, obeg, V + 1, st));
-    }
+    tb = tmpb;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, outcnt, obeg, V + 1, st));
     CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
-    k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, seen);
+    k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, counters);
     ++g_mp_launches;
-    int h_seen = 0;
-    CK(cudaMemcpyAsync(&h_seen, seen, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (h_seen != V) {
-        rc = cset_err(err, MP_ERR_CYCLE, V - h_seen, 0, "graph contains a cycle");
-    }
-    // ---- trie + node states -----------------------------------------------------------
+
+    // ---- trie + node states + K1b DFS ---------------------------------------------------
     Trie trie{};
     trie.child = ar.take<int>(TN);
     trie.sibling = ar.take<int>(TN);
@@ -599,104 +722,118 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     s.seq = ar.take<int>(static_cast<size_t>(V) * Lmax);
     s.tag = ar.take<int>(V);
     s.visited = ar.take<unsigned char>(V);
-    int *stack = ar.take<int>(E + V + 8), *buf = ar.take<int>(E + V + 8);
+    const int stack_cap = E + V + 8;
+    int *stack = ar.take<int>(stack_cap), *buf = ar.take<int>(stack_cap);
     int *ntrie = ar.take<int>(4);
-    if (rc == MP_OK) {
-        k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
-        ++g_mp_launches;
-        k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, s);
-        ++g_mp_launches;
-        // ---- K1b: the ordered DFS ------------------------------------------------------
+    k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
+    ++g_mp_launches;
+    k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, s);
+    ++g_mp_launches;
+    const size_t dsm = dfs_smem_bytes(V, E, Lmax, TN, stack_cap);
+    if (dsm <= static_cast<size_t>(MP_SMEM_DYN_MAX)) {
+        if (!cx.smem_attr) {
+            CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs_smem),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
+            cx.smem_attr = true;
+        }
+        k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap);
+    } else {
         k_dfs<<<1, 32, 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf);
-        ++g_mp_launches;
-        // ---- K2: final partition + materialize -----------------------------------------
-        int *og_rep = ar.take<int>(V), *og_pos = ar.take<int>(V), *og_tag = ar.take<int>(V), *og_size = ar.take<int>(V);
-        int *is_rep = ar.take<int>(V + 1), *size_at = ar.take<int>(V + 1), *grp_index = ar.take<int>(V + 1);
-        int *mem_off = ar.take<int>(V + 1), *members = ar.take<int>(V), *grp_of = ar.take<int>(V);
-        k_final_partition<<<grid, 256, 0, st>>>(V, d_seq_beg, d_seq, d_tag, trie, s, og_rep, og_pos, og_tag, og_size);
-        ++g_mp_launches;
-        k_rep_flags<<<grid, 256, 0, st>>>(V, og_rep, og_size, is_rep, size_at);
-        ++g_mp_launches;
-        CK(cudaMemsetAsync(is_rep + V, 0, 4, st));
-        CK(cudaMemsetAsync(size_at + V, 0, 4, st));
-        size_t tb = tmpb;
-        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, is_rep, grp_index, V + 1, st));
-        tb = tmpb;
-        CK(cub::DeviceScan::ExclusiveSum(tmp, tb, size_at, mem_off, V + 1, st));
-        k_scatter<<<grid, 256, 0, st>>>(V, og_rep, og_pos, grp_index, mem_off, members, grp_of);
-        ++g_mp_launches;
-        int ng = 0;
-        CK(cudaMemcpyAsync(&ng, grp_index + V, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        int *grp_node = ar.take<int>(V), *grp_tag = ar.take<int>(V), *grp_beg = ar.take<int>(V + 1);
-        long long *grp_mem = ar.take<long long>(V);
-        double *grp_cost = ar.take<double>(static_cast<size_t>(V) * D);
-        k_group_values<<<grid, 256, 0, st>>>(V, D, is_rep, grp_index, mem_off, og_tag, og_size, members, d_mem, d_cost,
-                                             d_seq_beg, d_seq, O, d_obeg, d_ot, d_odev, d_otime, in->sum_mode, grp_node,
-                                             grp_tag, grp_beg, grp_mem, grp_cost);
-        ++g_mp_launches;
-        // quotient edges (fusion.py:242-247): keys (gu, gv) sorted, payloads summed
-        unsigned long long *ekeys = keys, *eskeys = skeys, *ukeys = ar.take<unsigned long long>(E);
-        long long *evals = ar.take<long long>(E), *esvals = ar.take<long long>(E), *usum = ar.take<long long>(E);
-        int *nkeep = ar.take<int>(4), *nuniq = ar.take<int>(4);
-        CK(cudaMemsetAsync(nkeep, 0, 4, st));
-        CK(cudaMemsetAsync(nuniq, 0, 4, st));
-        int h_keep = 0, h_uniq = 0;
-        if (E) {
-            k_edge_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, grp_of, d_pay, ekeys, evals, nkeep);
-            ++g_mp_launches;
-            tb = tmpb;
-            CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ekeys, eskeys, evals, esvals, E, 0, 64, st));
-            CK(cudaMemcpyAsync(&h_keep, nkeep, 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (h_keep > 0) {
-                tb = tmpb;
-                CK(cub::DeviceReduce::ReduceByKey(tmp, tb, eskeys, ukeys, esvals, usum, nuniq, cub::Sum(), h_keep, st));
-                CK(cudaMemcpyAsync(&h_uniq, nuniq, 4, cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-            }
-        }
-        int *eu = ar.take<int>(std::max(h_uniq, 1));
-        int *ev = ar.take<int>(std::max(h_uniq, 1));
-        if (ar.used > ar.cap) {
-            rc = cset_err(err, MP_ERR_UNSUPPORTED, static_cast<int64_t>(ar.used), static_cast<int64_t>(ar.cap),
-                          "internal arena overflow");
-        } else {
-            if (h_uniq > 0) {
-                k_edge_split<<<grid, 256, 0, st>>>(h_uniq, ukeys, eu, ev);
-                ++g_mp_launches;
-            }
-            CK(cudaGetLastError());
-            // ---- download ---------------------------------------------------------------
-            out->n_groups = ng;
-            out->n_edges = h_uniq;
-            out->grp_node = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
-            out->grp_tag = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
-            out->mem_beg = static_cast<int32_t *>(malloc(4ULL * (ng + 1)));
-            out->members = static_cast<int32_t *>(malloc(4ULL * std::max(V, 1)));
-            out->grp_mem = static_cast<int64_t *>(malloc(8ULL * std::max(ng, 1)));
-            out->grp_cost = static_cast<double *>(malloc(8ULL * std::max(ng, 1) * D));
-            out->out_src = static_cast<int32_t *>(malloc(4ULL * std::max(h_uniq, 1)));
-            out->out_dst = static_cast<int32_t *>(malloc(4ULL * std::max(h_uniq, 1)));
-            out->out_payload = static_cast<int64_t *>(malloc(8ULL * std::max(h_uniq, 1)));
-            CK(cudaMemcpyAsync(out->grp_node, grp_node, 4ULL * ng, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->grp_tag, grp_tag, 4ULL * ng, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->mem_beg, grp_beg, 4ULL * ng, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->members, members, 4ULL * V, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->grp_mem, grp_mem, 8ULL * ng, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->grp_cost, grp_cost, 8ULL * ng * D, cudaMemcpyDeviceToHost, st));
-            if (h_uniq > 0) {
-                CK(cudaMemcpyAsync(out->out_src, eu, 4ULL * h_uniq, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(out->out_dst, ev, 4ULL * h_uniq, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(out->out_payload, usum, 8ULL * h_uniq, cudaMemcpyDeviceToHost, st));
-            }
-            CK(cudaStreamSynchronize(st));
-            out->mem_beg[ng] = V;
-        }
     }
-    cudaFree(ar.base);
-    cudaStreamDestroy(st);
-    return rc;
+    ++g_mp_launches;
+
+    // ---- K2: final partition + materialize ------------------------------------------------
+    int *og_rep = ar.take<int>(V), *og_pos = ar.take<int>(V), *og_tag = ar.take<int>(V), *og_size = ar.take<int>(V);
+    int *is_rep = ar.take<int>(V + 1), *size_at = ar.take<int>(V + 1), *grp_index = ar.take<int>(V + 1);
+    int *mem_off = ar.take<int>(V + 1), *members = ar.take<int>(V), *grp_of = ar.take<int>(V);
+    k_final_partition<<<grid, 256, 0, st>>>(V, d_seq_beg, d_seq, d_tag, trie, s, og_rep, og_pos, og_tag, og_size);
+    ++g_mp_launches;
+    k_rep_flags<<<grid, 256, 0, st>>>(V, og_rep, og_size, is_rep, size_at);
+    ++g_mp_launches;
+    CK(cudaMemsetAsync(is_rep + V, 0, 4, st));
+    CK(cudaMemsetAsync(size_at + V, 0, 4, st));
+    tb = tmpb;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, is_rep, grp_index, V + 1, st));
+    tb = tmpb;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, size_at, mem_off, V + 1, st));
+    k_scatter<<<grid, 256, 0, st>>>(V, og_rep, og_pos, grp_index, mem_off, members, grp_of);
+    ++g_mp_launches;
+    int *grp_node = ar.take<int>(V), *grp_tag = ar.take<int>(V), *grp_beg = ar.take<int>(V + 1);
+    long long *grp_mem = ar.take<long long>(V);
+    double *grp_cost = ar.take<double>(static_cast<size_t>(V) * D);
+    k_group_values<<<grid, 256, 0, st>>>(V, D, is_rep, grp_index, mem_off, og_tag, og_size, members, d_mem, d_cost,
+                                         d_seq_beg, d_seq, O, d_obeg, d_ot, d_odev, d_otime, in->sum_mode, grp_node,
+                                         grp_tag, grp_beg, grp_mem, grp_cost);
+    ++g_mp_launches;
+    // quotient edges (fusion.py:242-247): (gu, gv) keys radix-sorted, payloads summed per
+    // key; internal edges carry key ~0 and form one trailing segment that is dropped.
+    unsigned long long *ukeys = ar.take<unsigned long long>(E + 1);
+    long long *evals = ar.take<long long>(E), *esvals = ar.take<long long>(E), *usum = ar.take<long long>(E + 1);
+    int *eu = ar.take<int>(E + 1), *ev = ar.take<int>(E + 1);
+    if (E) {
+        k_edge_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, grp_of, d_pay, keys, evals, counters + 2);
+        ++g_mp_launches;
+        tb = tmpb;
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, evals, esvals, E, 0, 64, st));
+        tb = tmpb;
+        CK(cub::DeviceReduce::ReduceByKey(tmp, tb, skeys, ukeys, esvals, usum, counters + 1, cub::Sum(), E, st));
+        k_edge_split<<<grid, 256, 0, st>>>(counters + 1, ukeys, eu, ev);
+        ++g_mp_launches;
+    }
+    if (ar.used > ar.cap)
+        return cset_err(err, MP_ERR_UNSUPPORTED, static_cast<int64_t>(ar.used), static_cast<int64_t>(ar.cap),
+                        "internal arena overflow");
+    CK(cudaGetLastError());
+
+    // ---- one packed download -------------------------------------------------------------
+    size_t q = 0;
+    auto dl = [&](const void *src, size_t bytes) -> size_t {
+        const size_t at = (q + 255) & ~size_t(255);
+        q = at + bytes;
+        if (bytes) cudaMemcpyAsync(pin + at, src, bytes, cudaMemcpyDeviceToHost, st);
+        return at;
+    };
+    const size_t p_cnt = dl(counters, 64);
+    const size_t p_gidx = dl(grp_index + V, 4);
+    const size_t p_node = dl(grp_node, 4ULL * V);
+    const size_t p_tag = dl(grp_tag, 4ULL * V);
+    const size_t p_beg = dl(grp_beg, 4ULL * V);
+    const size_t p_mem = dl(members, 4ULL * V);
+    const size_t p_gmem = dl(grp_mem, 8ULL * V);
+    const size_t p_cost = dl(grp_cost, 8ULL * V * D);
+    const size_t p_eu = dl(eu, 4ULL * E);
+    const size_t p_ev = dl(ev, 4ULL * E);
+    const size_t p_sum = dl(usum, 8ULL * E);
+    const size_t p_ukey = dl(ukeys, 8ULL * E);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    const int *cnt = reinterpret_cast<const int *>(pin + p_cnt);
+    if (cnt[0] != V) return cset_err(err, MP_ERR_CYCLE, V - cnt[0], 0, "graph contains a cycle");
+    const int ng = *reinterpret_cast<const int *>(pin + p_gidx);
+    int nu = E ? cnt[1] : 0;
+    if (nu > 0 && reinterpret_cast<const unsigned long long *>(pin + p_ukey)[nu - 1] == ~0ULL) --nu;
+    out->n_groups = ng;
+    out->n_edges = nu;
+    out->grp_node = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
+    out->grp_tag = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
+    out->mem_beg = static_cast<int32_t *>(malloc(4ULL * (ng + 1)));
+    out->members = static_cast<int32_t *>(malloc(4ULL * std::max(V, 1)));
+    out->grp_mem = static_cast<int64_t *>(malloc(8ULL * std::max(ng, 1)));
+    out->grp_cost = static_cast<double *>(malloc(8ULL * std::max(ng, 1) * D));
+    out->out_src = static_cast<int32_t *>(malloc(4ULL * std::max(nu, 1)));
+    out->out_dst = static_cast<int32_t *>(malloc(4ULL * std::max(nu, 1)));
+    out->out_payload = static_cast<int64_t *>(malloc(8ULL * std::max(nu, 1)));
+    memcpy(out->grp_node, pin + p_node, 4ULL * ng);
+    memcpy(out->grp_tag, pin + p_tag, 4ULL * ng);
+    memcpy(out->mem_beg, pin + p_beg, 4ULL * ng);
+    out->mem_beg[ng] = V;
+    memcpy(out->members, pin + p_mem, 4ULL * V);
+    memcpy(out->grp_mem, pin + p_gmem, 8ULL * ng);
+    memcpy(out->grp_cost, pin + p_cost, 8ULL * ng * D);
+    memcpy(out->out_src, pin + p_eu, 4ULL * nu);
+    memcpy(out->out_dst, pin + p_ev, 4ULL * nu);
+    memcpy(out->out_payload, pin + p_sum, 8ULL * nu);
+    return MP_OK;
 }
 
 extern "C" void mp_coarsen_free(mp_coarsen_output *out) {

@@ -174,7 +174,8 @@ struct LaunchShape {
     int threads;
     int ctas;
     int smem;             // dynamic smem bytes
-    bool onchip;
+    bool onchip;          // state slots in shared memory (mode >= 1)
+    int mode;             // 2: tables + state in smem, 1: state in smem, 0: all global
 };
 
 // Launches one evaluator variant; returns cudaError_t of the launch.
@@ -185,5 +186,6 @@ cudaError_t mp_launch_finalize(const double *cta_ms, const long long *cta_row, i
 cudaError_t mp_launch_ls(const LaunchShape &shape, const EvalArgs &a, const LsArgs &ls, cudaStream_t s);
 cudaError_t mp_launch_ls_pick(const double *chain_ms, long long n, double *out_ms, long long *out_c,
                               cudaStream_t s);
+cudaError_t mp_launch_memcheck(const EvalArgs &a, long long *feas, unsigned int *n_feas, int sms, cudaStream_t s);
 cudaError_t mp_eval_set_smem_limits();
 extern unsigned long long g_mp_launches;

@@ -448,14 +448,20 @@ __device__ __forceinline__ void cta_keep_best(const EvalArgs &a, double best_ms,
     }
 }
 
+// MODE 2: tables staged into shared memory + state slots in shared memory;
+// MODE 1: state slots in shared memory, tables read from global (L1/L2);
+// MODE 0: both in global memory (huge instances).
 // grp == groups_per_cta is the dummy slot shared by idle lanes (lane >= U).
-template <bool ONCHIP>
+template <int MODE>
 __device__ __forceinline__ void group_bases(unsigned char *sm, const EvalArgs &a, int grp, uint64_t *bar,
                                             const unsigned char *&tb, unsigned char *&st) {
-    if constexpr (ONCHIP) {
+    if constexpr (MODE == 2) {
         stage_tables(sm, a, bar);
         tb = sm;
         st = sm + a.to.bytes + static_cast<size_t>(grp) * a.so.bytes;
+    } else if constexpr (MODE == 1) {
+        tb = a.blob;
+        st = sm + static_cast<size_t>(grp) * a.so.bytes;
     } else {
         tb = a.blob;
         st = a.gstate + (static_cast<size_t>(blockIdx.x) * (a.groups_per_cta + 1) + grp) * a.so.bytes;
@@ -471,7 +477,7 @@ __device__ __forceinline__ int group_of_lane(const EvalArgs &a, int lane, bool &
 }  // namespace
 
 // ---- K3/K4: batch evaluation with fused keep-best ---------------------------------
-template <int G, int SRC, bool ONCHIP, bool TRACE, bool COLO>
+template <int G, int SRC, int MODE, bool TRACE, bool COLO>
 __global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_eval_kernel(const __
     const int GPW = a.lanes_used / G;  // groups per warp
     const unsigned char *tb;
     unsigned char *st;
-    group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
+    group_bases<MODE>(sm, a, grp, &s_bar, tb, st);
     unsigned char *devbuf = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) devbuf[i] = 0;
     double best_ms = kInf;
@@ -561,7 +567,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 // capacity) counts as rejected; every makespan a chain carries is
 // an exact evaluation.  Results are identical for any G or GPU count at a fixed
 // ready capacity.
-template <int G, bool ONCHIP, bool COLO>
+template <int G, int MODE, bool COLO>
 __global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                      const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_ls_kernel(const __gr
     const int GPW = a.lanes_used / G;
     const unsigned char *tb;
     unsigned char *st;
-    group_bases<ONCHIP>(sm, a, grp, &s_bar, tb, st);
+    group_bases<MODE>(sm, a, grp, &s_bar, tb, st);
     unsigned char *dev = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) dev[i] = 0;
     const int n = a.n_ops, K = a.K;
@@ -692,42 +698,114 @@ typedef void (*EvalFn)(const EvalArgs);
 typedef void (*LsFn)(const EvalArgs, const LsArgs);
 
 template <int G, bool COLO>
-EvalFn pick_g(int src, bool onchip, bool trace) {
-    if (trace) return mp_eval_kernel<G, SRC_LOAD, false, true, COLO>;
-    if (src == SRC_LOAD)
-        return onchip ? mp_eval_kernel<G, SRC_LOAD, true, false, COLO> : mp_eval_kernel<G, SRC_LOAD, false, false, COLO>;
-    return onchip ? mp_eval_kernel<G, SRC_ENUM, true, false, COLO> : mp_eval_kernel<G, SRC_ENUM, false, false, COLO>;
-}
-
-template <bool COLO>
-EvalFn pick_c(int G, int src, bool onchip, bool trace) {
-    switch (G) {
-        case 1: return pick_g<1, COLO>(src, onchip, trace);
-        case 2: return pick_g<2, COLO>(src, onchip, trace);
-        case 4: return pick_g<4, COLO>(src, onchip, trace);
-        case 8: return pick_g<8, COLO>(src, onchip, trace);
-        case 16: return pick_g<16, COLO>(src, onchip, trace);
-        default: return pick_g<32, COLO>(src, onchip, trace);
+EvalFn pick_g(int src, int mode, bool trace) {
+    if (trace) return mp_eval_kernel<G, SRC_LOAD, 0, true, COLO>;
+    if (src == SRC_LOAD) {
+        switch (mode) {
+            case 2: return mp_eval_kernel<G, SRC_LOAD, 2, false, COLO>;
+            case 1: return mp_eval_kernel<G, SRC_LOAD, 1, false, COLO>;
+            default: return mp_eval_kernel<G, SRC_LOAD, 0, false, COLO>;
+        }
+    }
+    switch (mode) {
+        case 2: return mp_eval_kernel<G, SRC_ENUM, 2, false, COLO>;
+        case 1: return mp_eval_kernel<G, SRC_ENUM, 1, false, COLO>;
+        default: return mp_eval_kernel<G, SRC_ENUM, 0, false, COLO>;
     }
 }
 
-EvalFn pick_any(int G, int src, bool onchip, bool trace, bool colo) {
-    return colo ? pick_c<true>(G, src, onchip, trace) : pick_c<false>(G, src, onchip, trace);
-}
-
 template <bool COLO>
-LsFn pick_ls_c(int G, bool onchip) {
+EvalFn pick_c(int G, int src, int mode, bool trace) {
     switch (G) {
-        case 1: return onchip ? mp_ls_kernel<1, true, COLO> : mp_ls_kernel<1, false, COLO>;
-        case 2: return onchip ? mp_ls_kernel<2, true, COLO> : mp_ls_kernel<2, false, COLO>;
-        case 4: return onchip ? mp_ls_kernel<4, true, COLO> : mp_ls_kernel<4, false, COLO>;
-        case 8: return onchip ? mp_ls_kernel<8, true, COLO> : mp_ls_kernel<8, false, COLO>;
-        case 16: return onchip ? mp_ls_kernel<16, true, COLO> : mp_ls_kernel<16, false, COLO>;
-        default: return onchip ? mp_ls_kernel<32, true, COLO> : mp_ls_kernel<32, false, COLO>;
+        case 1: return pick_g<1, COLO>(src, mode, trace);
+        case 2: return pick_g<2, COLO>(src, mode, trace);
+        case 4: return pick_g<4, COLO>(src, mode, trace);
+        case 8: return pick_g<8, COLO>(src, mode, trace);
+        case 16: return pick_g<16, COLO>(src, mode, trace);
+        default: return pick_g<32, COLO>(src, mode, trace);
     }
 }
 
-LsFn pick_ls(int G, bool onchip, bool colo) { return colo ? pick_ls_c<true>(G, onchip) : pick_ls_c<false>(G, onchip); }
+EvalFn pick_any(int G, int src, int mode, bool trace, bool colo) {
+    return colo ? pick_c<true>(G, src, mode, trace) : pick_c<false>(G, src, mode, trace);
+}
+
+template <int G, bool COLO>
+LsFn pick_ls_g(int mode) {
+    switch (mode) {
+        case 2: return mp_ls_kernel<G, 2, COLO>;
+        case 1: return mp_ls_kernel<G, 1, COLO>;
+        default: return mp_ls_kernel<G, 0, COLO>;
+    }
+}
+
+template <bool COLO>
+LsFn pick_ls_c(int G, int mode) {
+    switch (G) {
+        case 1: return pick_ls_g<1, COLO>(mode);
+        case 2: return pick_ls_g<2, COLO>(mode);
+        case 4: return pick_ls_g<4, COLO>(mode);
+        case 8: return pick_ls_g<8, COLO>(mode);
+        case 16: return pick_ls_g<16, COLO>(mode);
+        default: return pick_ls_g<32, COLO>(mode);
+    }
+}
+
+LsFn pick_ls(int G, int mode, bool colo) { return colo ? pick_ls_c<true>(G, mode) : pick_ls_c<false>(G, mode); }
+
+// ---- memory-feasibility prefilter (solver.py:82-87) ------------------------------------
+// One warp per row: writes the result of infeasible rows and appends the global
+// index of every feasible row to `feas` for the scheduling pass (row_list mode).
+__global__ void __launch_bounds__(256) mp_memcheck_kernel(const EvalArgs a, long long *feas, unsigned int *n_feas) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const long long *mem = reinterpret_cast<const long long *>(a.blob + a.to.mem);
+    const long long *cap = reinterpret_cast<const long long *>(a.blob + a.to.cap);
+    const int K = a.K, n = a.n_ops;
+    for (long long p = warp; p < a.n_rows; p += nw) {
+        const uint8_t *row = a.rows + p * n;
+        unsigned long long acc[MP_MAX_DEV];
+#pragma unroll
+        for (int k = 0; k < MP_MAX_DEV; ++k) acc[k] = 0;
+        bool bad = false;
+        for (int i = lane; i < n; i += 32) {
+            const int d = row[i];
+            const unsigned long long m = static_cast<unsigned long long>(__ldg(mem + i));
+            bad |= d >= K;
+#pragma unroll
+            for (int k = 0; k < MP_MAX_DEV; ++k) acc[k] += (d == k) ? m : 0ULL;
+        }
+        bad = __any_sync(kFull, bad);
+#pragma unroll
+        for (int k = 0; k < MP_MAX_DEV; ++k)
+            for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], o);
+        if (lane == 0) {
+            int over = -1;
+            long long by = 0;
+            if (!bad) {
+#pragma unroll
+                for (int k = 0; k < MP_MAX_DEV; ++k) {
+                    if (k < K && over < 0 && static_cast<long long>(acc[k]) > cap[k]) {
+                        over = k;
+                        by = static_cast<long long>(acc[k]) - cap[k];
+                    }
+                }
+            }
+            const long long grow = a.row_base + p;
+            const long long o = grow - a.out_base;
+            if (bad || over >= 0) {
+                if (a.makespan) a.makespan[o] = kInf;
+                if (a.status) a.status[o] = bad ? MP_ROW_BAD_DEVICE : MP_ROW_MEMORY;
+                if (a.mem_dev) a.mem_dev[o] = bad ? -1 : over;
+                if (a.overflow) a.overflow[o] = bad ? 0 : by;
+            } else {
+                feas[atomicAdd(n_feas, 1u)] = grow;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t mp_eval_set_smem_limits() {
@@ -736,15 +814,17 @@ cudaError_t mp_eval_set_smem_limits() {
     const int Gs[6] = {1, 2, 4, 8, 16, 32};
     for (int gi = 0; gi < 6; ++gi) {
         for (int colo = 0; colo < 2; ++colo) {
-            for (int src = 0; src < 2; ++src) {
-                EvalFn f = pick_any(Gs[gi], src, true, false, colo != 0);
-                cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
+            for (int mode = 1; mode <= 2; ++mode) {
+                for (int src = 0; src < 2; ++src) {
+                    EvalFn f = pick_any(Gs[gi], src, mode, false, colo != 0);
+                    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+                    if (e != cudaSuccess) return e;
+                }
+                cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(pick_ls(Gs[gi], mode, colo != 0)),
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
                 if (e != cudaSuccess) return e;
             }
-            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(pick_ls(Gs[gi], true, colo != 0)),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
-            if (e != cudaSuccess) return e;
         }
     }
     done = true;
@@ -752,15 +832,22 @@ cudaError_t mp_eval_set_smem_limits() {
 }
 
 cudaError_t mp_launch_eval(const LaunchShape &ls, int src_mode, bool trace, const EvalArgs &a, cudaStream_t s) {
-    EvalFn f = pick_any(ls.G, src_mode, ls.onchip && !trace, trace, a.colo != 0);
-    f<<<ls.ctas, ls.threads, (ls.onchip && !trace) ? ls.smem : 0, s>>>(a);
+    const int mode = trace ? 0 : ls.mode;
+    EvalFn f = pick_any(ls.G, src_mode, mode, trace, a.colo != 0);
+    f<<<ls.ctas, ls.threads, mode ? ls.smem : 0, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
 }
 
 cudaError_t mp_launch_ls(const LaunchShape &shape, const EvalArgs &a, const LsArgs &ls, cudaStream_t s) {
-    LsFn f = pick_ls(shape.G, shape.onchip, a.colo != 0);
-    f<<<shape.ctas, shape.threads, shape.onchip ? shape.smem : 0, s>>>(a, ls);
+    LsFn f = pick_ls(shape.G, shape.mode, a.colo != 0);
+    f<<<shape.ctas, shape.threads, shape.mode ? shape.smem : 0, s>>>(a, ls);
+    ++g_mp_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t mp_launch_memcheck(const EvalArgs &a, long long *feas, unsigned int *n_feas, int sms, cudaStream_t s) {
+    mp_memcheck_kernel<<<sms * 8, 256, 0, s>>>(a, feas, n_feas);
     ++g_mp_launches;
     return cudaGetLastError();
 }

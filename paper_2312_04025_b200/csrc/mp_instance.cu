@@ -304,6 +304,8 @@ struct mp_instance {
     int sms = 0;
     int rcap_target = 32;
     int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
+    bool prefilter = false;  // memory-feasibility pass + compaction before scheduling
+    DevBuf feas_rows;
     TabOff to{};
     unsigned char *blob = nullptr;
     // main (on-chip when possible) and off-chip variants
@@ -333,18 +335,32 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     // Ready sets are antichains of the augmented DAG, so a vertex-disjoint path
     // cover bounds them: every non-sink op continues into one out-flow and every
     // non-source op is continued by one in-flow -> n_flows - n_ops + n_src + n_sinks
-    // paths.  On chip the capacity is min(bound, target): rows whose ready set
-    // outgrows it are re-run by the off-chip variant with capacity = bound.
-    int rcap = std::max(1, std::min(I->ready_bound, I->rcap_target));
-    StOff so = make_stoff(n_ops, I->n_multi, K, rcap);
+    // paths.  The main variant's capacity is min(bound, target) (target = 2x the
+    // calibration peak): rows whose ready set outgrows it are re-run by the
+    // off-chip variant with capacity = bound.
+    const int rcap = std::max(1, std::min(I->ready_bound, I->rcap_target));
+    const StOff so = make_stoff(n_ops, I->n_multi, K, rcap);
     // lanes per placement from the typical ready-set size: a lane holds about one entry
     const int typical = I->peak_probe > 0 ? I->peak_probe : I->ready_bound;
     const int G = G_req > 0 ? G_req : (typical <= 8 ? 4 : (typical <= 32 ? 8 : (typical <= 96 ? 16 : 32)));
-    // slots that fit next to the tables (one extra dummy slot for idle lanes)
-    const long long avail = static_cast<long long>(smem_cap) - I->to.bytes;
-    const long long slots = avail > 0 ? avail / so.bytes - 1 : 0;
+    // slots that fit (one extra dummy slot for idle lanes): with the tables staged
+    // in shared memory (mode 2) or read from global memory (mode 1)
+    const long long slots2 = std::max(0LL, (smem_cap - static_cast<long long>(I->to.bytes)) / so.bytes - 1);
+    const long long slots1 = std::max(0LL, static_cast<long long>(smem_cap) / so.bytes - 1);
+    int mode = 0;
+    long long slots = 0;
+    if (slots2 >= 1 && 4 * slots2 >= 3 * slots1) {
+        mode = 2;
+        slots = slots2;
+    } else if (slots1 * G >= 128) {  // >= 4 warps' worth of lanes
+        mode = 1;
+        slots = slots1;
+    } else if (slots2 >= 1 && slots2 * G >= 128) {
+        mode = 2;
+        slots = slots2;
+    }
     int best_U = 0, best_w = 0;
-    for (int U = 32; U >= G; U /= 2) {
+    for (int U = 32; U >= G && mode > 0; U /= 2) {
         if (U_req > 0 && U != U_req) continue;
         const int gpw = U / G;
         const int w = static_cast<int>(std::min<long long>(slots / gpw, MP_CTA_MAX_THREADS / 32));
@@ -353,14 +369,15 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
             best_w = w;
         }
     }
-    if (best_w >= 1) {
+    if (mode > 0 && best_w >= 1) {
         LaunchShape ls{};
         ls.G = G;
         ls.U = best_U;
         ls.threads = best_w * 32;
         ls.groups_per_cta = best_w * (best_U / G);
-        ls.smem = static_cast<int>(I->to.bytes + static_cast<long long>(ls.groups_per_cta + 1) * so.bytes);
+        ls.smem = static_cast<int>((mode == 2 ? I->to.bytes : 0) + static_cast<long long>(ls.groups_per_cta + 1) * so.bytes);
         ls.onchip = true;
+        ls.mode = mode;
         // static smem of the kernel is ~9 KB; 228 KB per SM in total
         int per_sm = std::max(1, (228 * 1024) / (ls.smem + 10 * 1024));
         per_sm = std::min(per_sm, 2048 / ls.threads);
@@ -369,10 +386,8 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
         I->main = ls;
         I->main_so = so;
         I->main_rcap = rcap;
-    } else {
-        I->main.onchip = false;
     }
-    // off-chip variant: one warp per placement, full ready capacity
+    // off-chip re-run variant: one warp per placement, capacity = bound
     StOff wso = make_stoff(n_ops, I->n_multi, K, std::max(1, I->ready_bound));
     LaunchShape w{};
     w.G = 32;
@@ -380,6 +395,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     w.threads = 256;
     w.groups_per_cta = 8;
     w.onchip = false;
+    w.mode = 0;
     w.smem = 0;
     // bound the scratch to ~8 GiB
     long long groups = static_cast<long long>(I->sms) * 8;
@@ -388,10 +404,18 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     w.ctas = static_cast<int>(std::max(1LL, groups / 8));
     I->wide = w;
     I->wide_so = wso;
-    if (!I->main.onchip) {
-        I->main = w;
-        I->main_so = wso;
-        I->main_rcap = std::max(1, I->ready_bound);
+    if (!(mode > 0 && best_w >= 1)) {
+        // huge instance: state in global memory too, capacity from the probe
+        LaunchShape m = w;
+        m.G = G_req > 0 ? G_req : 32;
+        m.U = 32;
+        m.groups_per_cta = 8 * (32 / m.G);
+        long long g2 = static_cast<long long>(I->sms) * m.groups_per_cta;
+        while (g2 > m.groups_per_cta && g2 * static_cast<long long>(so.bytes) > budget) g2 /= 2;
+        m.ctas = static_cast<int>(std::max(1LL, g2 / m.groups_per_cta));
+        I->main = m;
+        I->main_so = so;
+        I->main_rcap = rcap;
     }
 }
 
@@ -679,7 +703,7 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
             v = static_cast<uint8_t>(x % static_cast<unsigned long long>(K));
         }
         DevBuf pb;
-        MP_CUDA_I(pb.ensure(rows.size() + 64));
+        MP_CUDA_I(pb.ensure(rows.size() + 256));
         MP_CUDA_I(I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes));
         MP_CUDA_I(I->ctrs.ensure(64));
         MP_CUDA_I(I->ovf_rows.ensure(64));
@@ -694,11 +718,19 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
         a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
         a.peak_ready = reinterpret_cast<unsigned int *>(ctr + 4);
+        a.status = reinterpret_cast<int8_t *>(static_cast<unsigned char *>(pb.p) + rows.size());
         MP_CUDA_I(mp_launch_eval(I->wide, SRC_LOAD, false, a, I->stream));
         unsigned int peak = 0;
+        int8_t pst[128];
         MP_CUDA_I(cudaMemcpyAsync(&peak, ctr + 4, 4, cudaMemcpyDeviceToHost, I->stream));
+        MP_CUDA_I(cudaMemcpyAsync(pst, static_cast<unsigned char *>(pb.p) + rows.size(), P, cudaMemcpyDeviceToHost,
+                                  I->stream));
         MP_CUDA_I(cudaStreamSynchronize(I->stream));
         I->peak_probe = static_cast<int>(peak);
+        int infeasible = 0;
+        for (int r = 0; r < P; ++r) infeasible += pst[r] != MP_ROW_OK;
+        // most rows never reach the scheduler: check memory first, schedule the rest
+        I->prefilter = 4 * infeasible >= P;
         I->rcap_target = std::max(4, 2 * static_cast<int>(peak));
         choose_shapes(I, 0, 0, 0);
     }
@@ -742,6 +774,8 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->colo = I->colo ? 1 : 0;
     info->colo_ok = I->colo_ok ? 1 : 0;
     info->peak_probe = I->peak_probe;
+    info->prefilter = I->prefilter ? 1 : 0;
+    info->mode = I->main.mode;
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
     return MP_OK;
@@ -785,6 +819,10 @@ cudaError_t prepare(mp_instance *I, bool argmin, long long max_rows) {
         e = I->ovf_rows.ensure(static_cast<size_t>(std::max(1LL, max_rows)) * 8);
         if (e != cudaSuccess) return e;
     }
+    if (I->prefilter) {
+        e = I->feas_rows.ensure(static_cast<size_t>(std::max(1LL, max_rows)) * 8);
+        if (e != cudaSuccess) return e;
+    }
     (void)argmin;
     return cudaSuccess;
 }
@@ -825,6 +863,15 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
     a.next = ctr;
     a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
     a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    if (I->prefilter) {
+        // memory check + compaction first; only feasible rows reach the scheduler
+        unsigned int *nf = reinterpret_cast<unsigned int *>(ctr + 5);
+        if ((e = mp_launch_memcheck(a, static_cast<long long *>(I->feas_rows.p), nf, I->sms, s)) != cudaSuccess)
+            return e;
+        a.row_list = 1;
+        a.row_idx = static_cast<const long long *>(I->feas_rows.p);
+        a.n_rows_dev = nf;
+    }
     if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) return e;
     if (I->main_rcap < I->ready_bound) {
         // rows whose ready set outgrew the on-chip capacity: re-run off-chip

@@ -27,14 +27,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--rows", type=int, default=1 << 18)
-    ap.add_argument("--G", default="1:8,1:16,1:32,2:16,2:32,4:32,8:32", help="G or G:U list")
+    ap.add_argument("--G", default="0", help="G or G:U list (0 = automatic shape)")
     ap.add_argument("--rcap", type=int, default=0)
     ap.add_argument("--no-colo", action="store_true")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     args = ap.parse_args()
-    w = {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c2k8": lambda: workloads.c2(8),
-         "c3": workloads.c3, "c4": workloads.c4}[args.workload]()
+    if args.workload.startswith("c5:"):
+        _, n, k = args.workload.split(":")
+        w = workloads.c5(int(n), int(k))
+    else:
+        w = {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c2k8": lambda: workloads.c2(8),
+             "c3": workloads.c3, "c4": workloads.c4, "c4pcie": lambda: workloads.c4("pcie")}[args.workload]()
     coarse = mp.gcof(w.raw, w.rules)
     inst = mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster))
     rows = workloads.placements(w.seed, args.rows, inst.n_ops, inst.K)
@@ -70,7 +74,8 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         t = min(times)
-        print(f"{w.name} G={G} U={info['lanes_used']} colo={info['colo']} gpc={info['groups_per_cta']} "
+        feas = int((st == 0).sum().item())
+        print(f"{w.name} a={inst.n_ops} b={inst.n_flows} peak={info['peak_probe']} feasible={feas}/{args.rows} G={info['group_lanes']} U={info['lanes_used']} colo={info['colo']} gpc={info['groups_per_cta']} "
               f"ctas={info['ctas']} rcap={info['ready_cap']} smem={info['smem_bytes']} state={info['state_bytes']} "
               f"tables={info['table_bytes']}: {args.rows / t:,.0f} placements/s ({t * 1e3:.2f} ms) best={best.value}",
               flush=True)
