@@ -345,17 +345,20 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     const int G = G_req > 0 ? G_req : (typical <= 8 ? 4 : (typical <= 32 ? 8 : (typical <= 96 ? 16 : 32)));
     // slots that fit (one extra dummy slot for idle lanes): with the tables staged
     // in shared memory (mode 2) or read from global memory (mode 1)
-    const long long slots2 = std::max(0LL, (smem_cap - static_cast<long long>(I->to.bytes)) / so.bytes - 1);
-    const long long slots1 = std::max(0LL, static_cast<long long>(smem_cap) / so.bytes - 1);
+    // (the dummy slot is only needed when some lanes idle, i.e. U < 32; with
+    // G == 32 every lane owns a group)
+    const long long dummy = G == 32 ? 0 : 1;
+    const long long slots2 = std::max(0LL, (smem_cap - static_cast<long long>(I->to.bytes)) / so.bytes - dummy);
+    const long long slots1 = std::max(0LL, static_cast<long long>(smem_cap) / so.bytes - dummy);
     int mode = 0;
     long long slots = 0;
     if (slots2 >= 1 && 4 * slots2 >= 3 * slots1) {
         mode = 2;
         slots = slots2;
-    } else if (slots1 * G >= 128) {  // >= 4 warps' worth of lanes
+    } else if (slots1 * G >= 128) {  // >= 4 warps of lanes at shared-memory latency
         mode = 1;
         slots = slots1;
-    } else if (slots2 >= 1 && slots2 * G >= 128) {
+    } else if (slots2 >= 1 && slots2 * G >= 64) {
         mode = 2;
         slots = slots2;
     }
@@ -375,7 +378,8 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
         ls.U = best_U;
         ls.threads = best_w * 32;
         ls.groups_per_cta = best_w * (best_U / G);
-        ls.smem = static_cast<int>((mode == 2 ? I->to.bytes : 0) + static_cast<long long>(ls.groups_per_cta + 1) * so.bytes);
+        ls.smem = static_cast<int>((mode == 2 ? I->to.bytes : 0) +
+                                   static_cast<long long>(ls.groups_per_cta + (best_U < 32 ? 1 : 0)) * so.bytes);
         ls.onchip = true;
         ls.mode = mode;
         // static smem of the kernel is ~9 KB; 228 KB per SM in total

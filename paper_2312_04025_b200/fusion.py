@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import sys
+from itertools import chain
 from dataclasses import dataclass
 from enum import Enum
 from typing import Iterable, Iterator
@@ -21,7 +22,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import CycleError, UnknownEdgeError
-from .graph import CompGraph, FlowEdge, OpNode, Tag, find_cycle
+from .graph import CompGraph, FlowEdge, OpNode, Tag, _make_edge, _make_opnode, find_cycle
 from .profiles import CostOverrides
 
 FUSE_JOINER = "∘"  # joins member types in a fused node's op_type (fusion.py:23)
@@ -114,42 +115,51 @@ class _Flat:
     """Array form of a coarsening problem (mp_coarsen_input)."""
 
     def __init__(self, g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None):
-        types: dict[str, int] = {}
-
-        def tid(t: str) -> int:
-            v = types.get(t)
-            if v is None:
-                v = types[t] = len(types)
-            return v
-
         nodes = g.nodes
         dg = g.csr()
+        V = len(nodes)
+        seqs = [n.type_seq for n in nodes]
+        flat_types = list(chain.from_iterable(seqs))
+        for r in rules:
+            flat_types.extend(r.pattern)
+        if overrides is not None:
+            for (s, _k) in overrides.entries:
+                flat_types.extend(s)
+        types = {t: k for k, t in enumerate(dict.fromkeys(flat_types))}
+        lens = np.fromiter(map(len, seqs), dtype=np.int32, count=V)
+        seq_beg = np.zeros(V + 1, np.int32)
+        np.cumsum(lens, out=seq_beg[1:])
+        total = int(seq_beg[-1])
+        seq = np.fromiter((types[t] for t in flat_types[:total]), dtype=np.int32, count=total)
+        tag = np.fromiter((_TAG_CODE[n.tag] for n in nodes), dtype=np.int32, count=V)
+        mem = np.fromiter((n.mem_bytes for n in nodes), dtype=np.int64, count=V)
+        cts = [n.compute_time for n in nodes]
         devs = set()
-        for n in nodes:
-            devs.update(n.compute_time)
+        first = tuple(cts[0]) if cts else ()
+        uniform = all(tuple(ct) == first for ct in cts)
+        if uniform:
+            devs.update(first)
+        else:
+            for ct in cts:
+                devs.update(ct)
         if overrides is not None:
             devs.update(k for (_, k) in overrides.entries)
         self.devices = sorted(devs)
         dindex = {d: i for i, d in enumerate(self.devices)}
-        V, D = len(nodes), len(self.devices)
-        seq_beg = np.zeros(V + 1, np.int32)
-        seq = []
-        tag = np.empty(V, np.int32)
-        mem = np.empty(V, np.int64)
-        cost = np.full((V, max(D, 1)), np.nan)
-        for i, n in enumerate(nodes):
-            seq.extend(tid(t) for t in n.type_seq)
-            seq_beg[i + 1] = len(seq)
-            tag[i] = _TAG_CODE[n.tag]
-            mem[i] = n.mem_bytes
-            for k, t in n.compute_time.items():
-                cost[i, dindex[k]] = float(t)
+        D = len(self.devices)
+        if uniform and V and list(first) == self.devices:
+            cost = np.array([list(ct.values()) for ct in cts], dtype=np.float64).reshape(V, max(D, 1))
+        else:
+            cost = np.full((V, max(D, 1)), np.nan)
+            for i, ct in enumerate(cts):
+                for k, t in ct.items():
+                    cost[i, dindex[k]] = float(t)
         rb = np.zeros(len(rules) + 1, np.int32)
         rt = []
         rid = np.empty(len(rules), np.int32)
         for r, rule in enumerate(rules):
             rid[r] = rule.id
-            rt.extend(tid(t) for t in rule.pattern)
+            rt.extend(types[t] for t in rule.pattern)
             rb[r + 1] = len(rt)
         ob = [0]
         ot = []
@@ -157,12 +167,12 @@ class _Flat:
         otime = []
         if overrides is not None:
             for (s, k), t in overrides.entries.items():
-                ot.extend(tid(x) for x in s)
+                ot.extend(types[x] for x in s)
                 ob.append(len(ot))
                 odev.append(dindex[k])
                 otime.append(float(t))
         self.keep = [
-            dg.ids, seq_beg, np.asarray(seq or [0], np.int32), tag, mem, np.ascontiguousarray(cost),
+            dg.ids, seq_beg, seq if total else np.zeros(1, np.int32), tag, mem, np.ascontiguousarray(cost),
             dg.esrc, dg.edst, dg.payload, rid, rb, np.asarray(rt or [0], np.int32),
             np.asarray(ob, np.int32), np.asarray(ot or [0], np.int32), np.asarray(odev or [0], np.int32),
             np.asarray(otime or [0.0], np.float64),
@@ -212,20 +222,24 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         lib.mp_coarsen_free(C.byref(out))
     new_nodes = []
     gid_of = []
+    sizes = np.diff(mbeg)
+    mb = mbeg.tolist()
+    mlist = members.tolist()
+    devices = flat.devices
     for z in range(ng):
-        mem_idx = members[mbeg[z]:mbeg[z + 1]]
-        if len(mem_idx) == 1:
-            n = nodes_in[int(mem_idx[0])]
+        if sizes[z] == 1:
+            n = nodes_in[mlist[mb[z]]]
             new_nodes.append(n)
             gid_of.append(n.id)
             continue
-        parts = [nodes_in[int(m)] for m in mem_idx]
+        parts = [nodes_in[m] for m in mlist[mb[z]:mb[z + 1]]]
         seq = tuple(t for p in parts for t in p.type_seq)
         mids = tuple(x for p in parts for x in p.members)
-        cost = {flat.devices[k]: float(gcost[z, k]) for k in range(D) if not np.isnan(gcost[z, k])}
+        row = gcost[z].tolist()
+        cost = {devices[k]: row[k] for k in range(D) if row[k] == row[k]}
         gid = min(p.id for p in parts)
-        new_nodes.append(OpNode(gid, FUSE_JOINER.join(seq), int(gmem[z]), cost, mids, seq,
-                                _CODE_TAG[int(grp_tag[z])]))
+        new_nodes.append(_make_opnode(gid, FUSE_JOINER.join(seq), int(gmem[z]), cost, mids, seq,
+                                      _CODE_TAG[int(grp_tag[z])]))
         gid_of.append(gid)
-    edges = [FlowEdge(gid_of[int(u)], gid_of[int(v)], int(p)) for u, v, p in zip(esrc, edst, epay)]
-    return CompGraph(new_nodes, edges)
+    edges = [_make_edge(gid_of[u], gid_of[v], p) for u, v, p in zip(esrc.tolist(), edst.tolist(), epay.tolist())]
+    return CompGraph._trusted(new_nodes, edges)
