@@ -101,6 +101,7 @@ typedef struct mp_instance_info {
     int32_t peak_probe;         /* largest ready set on the creation-time calibration probe */
     int32_t prefilter;          /* 1: a memory-feasibility pass compacts rows before scheduling */
     int32_t mode;               /* 2: tables+state in smem, 1: state in smem, 0: all global */
+    int32_t fastdiv;            /* 1: payload/bw by verified reciprocal + Markstein step */
     int64_t table_bytes;        /* instance tables staged per CTA                    */
     int64_t state_bytes;        /* per-placement dynamic state                       */
 } mp_instance_info;

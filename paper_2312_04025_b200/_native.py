@@ -57,6 +57,7 @@ class mp_instance_info(C.Structure):
         ("smem_bytes", C.c_int32), ("onchip", C.c_int32), ("device", C.c_int32),
         ("n_multi", C.c_int32), ("ready_bound", C.c_int32), ("colo", C.c_int32), ("colo_ok", C.c_int32),
         ("peak_probe", C.c_int32), ("prefilter", C.c_int32), ("mode", C.c_int32),
+        ("fastdiv", C.c_int32),
         ("table_bytes", C.c_int64), ("state_bytes", C.c_int64),
     ]
 

@@ -25,11 +25,10 @@ struct TabOff {
     uint32_t cost;      // f64 [n_ops*K]    p[i][k]                       (solver.py:61)
     uint32_t mem;       // i64 [n_ops]      mem_bytes                     (solver.py:60)
     uint32_t bw;        // f64 [K*K]        effective bandwidth           (solver.py:66-67)
+    uint32_t rbw;       // f64 [K*K]        correctly rounded 1/bw (Markstein division)
+    uint32_t s_rec;     // 16 B [n_flows]   slot record {dst op, node id (n_ops + f), (double)payload}
     uint32_t cap;       // i64 [K]          device capacity               (solver.py:59)
     uint32_t out_beg;   // u32 [n_ops+1]    CSR over out-flow *slots* (flows stably sorted by source)
-    uint32_t s_dst;     // u32 [n_flows]    slot -> destination op
-    uint32_t s_fid;     // u32 [n_flows]    slot -> flow index (edge order; node = n_ops + f)
-    uint32_t s_pay;     // f64 [n_flows]    slot -> (double)payload_bytes (solver.py:65,77)
     uint32_t fdst;      // u32 [n_flows]    flow index -> destination op   (solver.py:64)
     uint32_t mi;        // u32 [n_ops]      op -> multi-input slot, or MP_NONE (in-degree <= 1)
     uint32_t m_op;      // u32 [n_multi]    multi-input slot -> op
@@ -66,6 +65,7 @@ struct EvalArgs {
     StOff so;
     int n_ops, n_flows, K, n_levels, n_src, n_multi, rcap;
     int colo;                     // skip co-located flows (exact when all durations > 0)
+    int fastdiv;                  // payload/bw via verified reciprocal + one Markstein correction
 
     // row source
     const uint8_t *rows;          // LOAD: [n_rows][n_ops]
@@ -156,6 +156,19 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
 }
 __device__ __forceinline__ double bitsd(unsigned long long b) {
     return __longlong_as_double(static_cast<long long>(b));
+}
+
+// payload / bw, bit-identical to IEEE division: q0 = a*y, r = a - b*q0 (exact
+// with an fma), q = q0 + r*y (Markstein).  Used only when the instance verified
+// it against IEEE division for every (payload, bandwidth) pair it can produce
+// (mp_instance.cu k_verify_div); otherwise the IEEE division routine runs.
+__device__ __forceinline__ double div_bw(double a, double b, double y, int fast) {
+    if (fast) {
+        const double q0 = __dmul_rn(a, y);
+        const double r = __fma_rn(-q0, b, a);
+        return __fma_rn(r, y, q0);
+    }
+    return a / b;
 }
 
 // Dispatch key order of the reference list scheduler (solver.py:126-129):

@@ -189,10 +189,10 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     // table bases (hoisted: one address computation per kernel, not per access)
     const double *__restrict__ T_cost = tab<double>(tb, a.to.cost);
     const double *__restrict__ T_bw = tab<double>(tb, a.to.bw);
+    const double *__restrict__ T_rbw = tab<double>(tb, a.to.rbw);
+    const double2 *__restrict__ T_rec = tab<double2>(tb, a.to.s_rec);  // {dst | node id, payload}
+    const int fast = a.fastdiv;
     const uint32_t *__restrict__ T_out_beg = tab<uint32_t>(tb, a.to.out_beg);
-    const uint32_t *__restrict__ T_s_dst = tab<uint32_t>(tb, a.to.s_dst);
-    const uint32_t *__restrict__ T_s_fid = tab<uint32_t>(tb, a.to.s_fid);
-    const double *__restrict__ T_s_pay = tab<double>(tb, a.to.s_pay);
     const uint32_t *__restrict__ T_fdst = tab<uint32_t>(tb, a.to.fdst);
     const uint32_t *__restrict__ T_mi = tab<uint32_t>(tb, a.to.mi);
 
@@ -207,11 +207,13 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             double best = 0.0;
             const int qe = static_cast<int>(T_out_beg[i + 1]);
             for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
-                const int j = static_cast<int>(T_s_dst[q]);
+                const double2 rec = T_rec[q];
+                const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
                 const int dj = dev[j];
                 // rank of the flow node = dur + rank[j]   (rank[j] >= +0.0)
                 const bool cross = dj != d;
-                const double dv = T_s_pay[q] / (cross ? T_bw[d * K + dj] : 1.0);
+                const int bi = cross ? d * K + dj : 0;
+                const double dv = div_bw(rec.y, cross ? T_bw[bi] : 1.0, cross ? T_rbw[bi] : 1.0, fast);
                 const double fr = cross ? dv + rank[j] : rank[j];
                 best = fr > best ? fr : best;
             }
@@ -348,16 +350,19 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int t = t0 + gl;
             const bool act = t < cnt;
             const int q = (act && isop) ? ob + t : 0;
-            const int j = static_cast<int>(isop ? T_s_dst[q] : jflow);
+            const double2 rec = T_rec[q];
+            const unsigned long long rb = dbits(rec.x);
+            const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
             const int dj = dev[j];
-            const uint32_t pid = isop ? static_cast<uint32_t>(n_ops) + T_s_fid[q] : static_cast<uint32_t>(node);
+            const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
             const bool cross = dj != d;
             const bool via_colo = COLO && isop && !cross;
             const bool flow_ins = act && isop && !via_colo;   // a flow enters the ready set
             const bool op_upd = act && !flow_ins;             // j's npred / est / gate change
             // flow entry (crossing: payload / bw; co-located without colo: 0.0)
             const bool fcross = isop && cross;
-            const double fdur = fcross ? T_s_pay[q] / T_bw[fcross ? d * K + dj : 0] : 0.0;
+            const int bi = fcross ? d * K + dj : 0;
+            const double fdur = fcross ? div_bw(rec.y, T_bw[bi], T_rbw[bi], fast) : 0.0;
             const double rj = rank[j];
             const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
                                                    (static_cast<uint32_t>(2 * K + dj) << 26))

@@ -93,8 +93,10 @@ __global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cos
         bcost[x] = c;
     }
     for (int i = t0; i < n_ops; i += stride) bmem[i] = mem[i];
+    double *brbw = reinterpret_cast<double *>(blob + to.rbw);
     for (int k = t0; k < K * K; k += stride) {
         bbw[k] = bw[k];
+        brbw[k] = (k / K != k % K) ? __drcp_rn(bw[k]) : 1.0;
         if (k / K != k % K) atomicMax(&be->max_bw_bits, static_cast<unsigned long long>(__double_as_longlong(bw[k])));
     }
     for (int k = t0; k < K; k += stride) bcap[k] = cap[k];
@@ -114,14 +116,34 @@ __global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cos
     }
 }
 
-// flow slots in source order: s_fid = sorted flow index, s_dst / s_pay gathered
-__global__ void k_slots(int n_flows, const unsigned int *sorted_f, const int *fdst, const double *pay_d,
+// flow slots in source order: one 16-byte record {dst | node id << 32, payload}
+__global__ void k_slots(int n_ops, int n_flows, const unsigned int *sorted_f, const int *fdst, const double *pay_d,
                         unsigned char *blob, TabOff to) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_flows; q += gridDim.x * blockDim.x) {
         const unsigned int f = sorted_f[q];
-        reinterpret_cast<uint32_t *>(blob + to.s_fid)[q] = f;
-        reinterpret_cast<uint32_t *>(blob + to.s_dst)[q] = static_cast<uint32_t>(fdst[f]);
-        reinterpret_cast<double *>(blob + to.s_pay)[q] = pay_d[f];
+        const unsigned long long w = static_cast<unsigned long long>(static_cast<uint32_t>(fdst[f])) |
+                                     (static_cast<unsigned long long>(static_cast<uint32_t>(n_ops) + f) << 32);
+        reinterpret_cast<double2 *>(blob + to.s_rec)[q] = make_double2(__longlong_as_double(static_cast<long long>(w)), pay_d[f]);
+    }
+}
+
+// Markstein division check: for every flow payload and ordered device pair the
+// instance can produce, q0 = a*y, q = fma(fma(-q0, b, a), y, q0) must equal the
+// IEEE quotient bit for bit; any mismatch disables the fast path.
+__global__ void k_verify_div(int n_flows, int K, const double *pay_d, const unsigned char *blob, TabOff to,
+                             unsigned int *mismatch) {
+    const double *bw = reinterpret_cast<const double *>(blob + to.bw);
+    const double *rbw = reinterpret_cast<const double *>(blob + to.rbw);
+    const long long total = static_cast<long long>(n_flows) * K * K;
+    for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
+         x += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int f = static_cast<int>(x / (K * K));
+        const int p = static_cast<int>(x % (K * K));
+        if (p / K == p % K) continue;
+        const double a = pay_d[f], b = bw[p];
+        const double fast = div_bw(a, b, rbw[p], 1);
+        const double slow = a / b;
+        if (__double_as_longlong(fast) != __double_as_longlong(slow)) atomicOr(mismatch, 1u);
     }
 }
 
@@ -259,11 +281,10 @@ TabOff make_taboff(int n_ops, int n_flows, int K) {
     t.cost = take(8ULL * n_ops * K);
     t.mem = take(8ULL * n_ops);
     t.bw = take(8ULL * K * K);
+    t.rbw = take(8ULL * K * K);
     t.cap = take(8ULL * K);
     t.out_beg = take(4ULL * (n_ops + 1));
-    t.s_dst = take(4ULL * n_flows);
-    t.s_fid = take(4ULL * n_flows);
-    t.s_pay = take(8ULL * n_flows);
+    t.s_rec = take(16ULL * n_flows);
     t.fdst = take(4ULL * n_flows);
     t.mi = take(4ULL * n_ops);
     t.m_op = take(4ULL * n_ops);   // n_multi <= n_ops
@@ -301,6 +322,7 @@ struct mp_instance {
     int ready_bound = 0;   // min-path-cover bound on any ready set
     bool colo_ok = false;  // every op cost and crossing-flow duration > 0
     bool colo = false;     // co-located flows skipped
+    bool fastdiv = false;  // Markstein division verified for this instance
     int sms = 0;
     int rcap_target = 32;
     int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
@@ -435,6 +457,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.n_src = I->n_src;
     a.n_multi = I->n_multi;
     a.colo = I->colo ? 1 : 0;
+    a.fastdiv = I->fastdiv ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
     a.lanes_used = wide ? I->wide.U : I->main.U;
@@ -635,7 +658,9 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         tb = tmpb;
         MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, reinterpret_cast<const unsigned int *>(raw_src), keys, iota,
                                                   sorted_f, n_flows, 0, 32, I->stream));
-        k_slots<<<gridN, 256, 0, I->stream>>>(n_flows, sorted_f, raw_dst, pay_d, I->blob, I->to);
+        k_slots<<<gridN, 256, 0, I->stream>>>(n_ops, n_flows, sorted_f, raw_dst, pay_d, I->blob, I->to);
+        ++g_mp_launches;
+        k_verify_div<<<gridN, 256, 0, I->stream>>>(n_flows, K, pay_d, I->blob, I->to, reinterpret_cast<unsigned int *>(nsel) + 2);
         ++g_mp_launches;
         tb = tmpb;
         MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, reinterpret_cast<const unsigned int *>(raw_dst), keys, iota,
@@ -672,10 +697,11 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     // initial ready set: ops without in-flows, ascending
     tb = tmpb;
     MP_CUDA_I(cub::DeviceSelect::Flagged(tmp, tb, iota, is_src, b_srcs, nsel, n_ops, I->stream));
-    int h_nsel = 0;
-    MP_CUDA_I(cudaMemcpyAsync(&h_nsel, nsel, sizeof(int), cudaMemcpyDeviceToHost, I->stream));
+    int h_nsel[4] = {0, 0, 0, 0};
+    MP_CUDA_I(cudaMemcpyAsync(h_nsel, nsel, sizeof(h_nsel), cudaMemcpyDeviceToHost, I->stream));
     MP_CUDA_I(cudaStreamSynchronize(I->stream));
-    I->n_src = h_nsel;
+    I->n_src = h_nsel[0];
+    I->fastdiv = h_nsel[2] == 0;
     I->n_sinks = static_cast<int>(be.n_sinks);
     I->ready_bound = std::min(I->n_nodes, n_flows - n_ops + I->n_src + I->n_sinks);
     // Skipping co-located flows is exact when every op cost and every crossing
@@ -780,6 +806,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->peak_probe = I->peak_probe;
     info->prefilter = I->prefilter ? 1 : 0;
     info->mode = I->main.mode;
+    info->fastdiv = I->fastdiv ? 1 : 0;
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
     return MP_OK;
