@@ -169,6 +169,28 @@ int32_t mp_local_search(mp_instance *inst, const uint8_t *seed_rows, int32_t n_s
                         uint64_t rng_seed, uint8_t *best_row, double *best_ms,
                         int64_t *best_chain, double *chain_ms, void *stream, mp_error *err);
 
+/* ---- Branch and bound (replaces solve_exact, solver.py:172-254) ----------
+ * Ops are branched in `op_order` (n_ops op indices = topo_order(gc),
+ * solver.py:72), devices ascending; memory-prefix check (:233-234), the
+ * reference's node bound (:197-215), strict incumbent rule (:225-230).  A round
+ * bounds up to 65536 children on the GPU at once; leaves are scheduled exactly.
+ * gap == 0: the optimum and, among optimal rows, the lexicographically smallest
+ * in op_order (= brute_force's first strict minimum) whatever the seeds.
+ * gap > 0: prune when bound >= best*(1-gap) (:239).  node_limit < 0 / time_limit_s
+ * < 0 mean unlimited; limits are checked between rounds.  `seed_rows` (may be
+ * NULL) are evaluated first as incumbent candidates.  solve_status receives
+ * MP_SOLVE_* (Status.OPTIMAL / FEASIBLE / INFEASIBLE / BUDGET, placement.py:12-16);
+ * best_row/best_ms are valid for OPTIMAL and FEASIBLE. */
+#define MP_SOLVE_OPTIMAL    0
+#define MP_SOLVE_FEASIBLE   1
+#define MP_SOLVE_INFEASIBLE 2
+#define MP_SOLVE_BUDGET     3
+int32_t mp_branch_and_bound(mp_instance *inst, const int32_t *op_order, double gap,
+                            int64_t node_limit, double time_limit_s,
+                            const uint8_t *seed_rows, int32_t n_seed,
+                            uint8_t *best_row, double *best_ms, int32_t *solve_status,
+                            int64_t *visited, mp_error *err);
+
 /* ---- GCOF coarsening (K1/K2; replaces gcof, fusion.py:271-304) ----------- */
 typedef struct mp_coarsen_input {
     int32_t n_nodes;            /* V: input op nodes in ascending id order          */

@@ -13,6 +13,8 @@
  *   orc_schedule      opplace/solver.py:80-148  (_schedule)
  *   orc_eval_batch    solver.py:271-279 inner loop (one _schedule per row), pthreads
  *   orc_enumerate     solver.py:257-282         (brute_force keep-best)
+ *   orc_solve_exact   solver.py:172-254         (solve_exact branch and bound, gap and
+ *                                                node limit; the time limit is not restated)
  *   orc_gcof          opplace/fusion.py:93-104,117-130,133-248,271-304 (gcof)
  *
  * Data conventions are those of include/moirai_b200.h: op index = ascending op
@@ -363,6 +365,129 @@ int64_t orc_enumerate(const orc_inst *I, const int32_t *op_order, double *best_m
     ws_free(&w);
     *best_ms = best;
     return bidx;
+}
+
+/* solve_exact (solver.py:172-254): depth-first branch and bound over ops in
+   op_order, devices ascending, with the reference's running per-device memory
+   and compute loads (the += / -= pairs of :232-242, whose floating-point drift is
+   reproduced), its lower bound (:197-215) and incumbent rule (:225-230).
+   Returns 0 OPTIMAL, 1 FEASIBLE (node limit hit), 2 INFEASIBLE, 3 BUDGET. */
+typedef struct {
+    const orc_inst *I;
+    const int32_t *order;
+    double gap;
+    int64_t node_limit, visited;
+    int stopped;
+    uint8_t *assign;     /* 255 = unassigned */
+    int64_t *load;
+    double *load_time, *down, *min_p;
+    double best_obj;
+    uint8_t *best_row;
+    int have_best;
+    orc_ws w;
+} bnb_ctx;
+
+static double bnb_lower_bound(bnb_ctx *c) {
+    const orc_inst *I = c->I;
+    const orc_problem *p = &I->p;
+    const int n = p->n_ops, K = p->K;
+    double cp = 0.0;
+    int have_cp = 0;
+    for (int t = 0; t < n; ++t) {
+        int i = I->rev_topo[t];
+        double best = 0.0;
+        for (int q = I->out_beg[i]; q < I->out_beg[i + 1]; ++q) {
+            int f = I->out_flow[q];
+            int j = p->fdst[f];
+            double wq = 0.0;
+            if (c->assign[i] != 255 && c->assign[j] != 255) {
+                int ka = c->assign[i], kb = c->assign[j];
+                wq = (ka == kb) ? 0.0 : (double)p->payload[f] / p->bw[ka * K + kb];
+            }
+            double bf = 0.0;
+            if (c->down[j] > bf) bf = c->down[j];
+            double df = wq + bf;
+            if (df > best) best = df;
+            if (!have_cp || df > cp) { cp = df; have_cp = 1; }
+        }
+        double wi = c->assign[i] != 255 ? p->cost[i * K + c->assign[i]] : c->min_p[i];
+        c->down[i] = wi + best;
+        if (!have_cp || c->down[i] > cp) { cp = c->down[i]; have_cp = 1; }
+    }
+    double busiest = c->load_time[0];
+    for (int k = 1; k < K; ++k)
+        if (c->load_time[k] > busiest) busiest = c->load_time[k];
+    return cp > busiest ? cp : busiest;
+}
+
+static void bnb_descend(bnb_ctx *c, int idx) {
+    const orc_problem *p = &c->I->p;
+    const int n = p->n_ops, K = p->K;
+    if (c->stopped) return;
+    c->visited++;
+    if (c->node_limit >= 0 && c->visited > c->node_limit) {
+        c->stopped = 1;
+        return;
+    }
+    if (idx == n) {
+        double ms;
+        schedule_ws(c->I, &c->w, c->assign, NULL, NULL, &ms, NULL, NULL);
+        if (ms < c->best_obj) {
+            c->best_obj = ms;
+            memcpy(c->best_row, c->assign, (size_t)n);
+            c->have_best = 1;
+        }
+        return;
+    }
+    int i = c->order[idx];
+    for (int k = 0; k < K && !c->stopped; ++k) {
+        if (c->load[k] + p->mem[i] > p->cap[k]) continue;
+        c->assign[i] = (uint8_t)k;
+        c->load[k] += p->mem[i];
+        c->load_time[k] += p->cost[i * K + k];
+        double lb = bnb_lower_bound(c);
+        if (!c->have_best || lb < c->best_obj * (1.0 - c->gap)) bnb_descend(c, idx + 1);
+        c->assign[i] = 255;
+        c->load[k] -= p->mem[i];
+        c->load_time[k] -= p->cost[i * K + k];
+    }
+}
+
+int orc_solve_exact(const orc_inst *I, const int32_t *op_order, double gap, int64_t node_limit, uint8_t *best_row,
+                    double *best_ms, int64_t *visited) {
+    const int n = I->p.n_ops, K = I->p.K;
+    bnb_ctx c;
+    memset(&c, 0, sizeof(c));
+    c.I = I;
+    c.order = op_order;
+    c.gap = gap;
+    c.node_limit = node_limit;
+    c.assign = (uint8_t *)malloc((size_t)n);
+    memset(c.assign, 255, (size_t)n);
+    c.load = (int64_t *)calloc((size_t)K, sizeof(int64_t));
+    c.load_time = (double *)calloc((size_t)K, sizeof(double));
+    c.down = (double *)calloc((size_t)n, sizeof(double));
+    c.min_p = (double *)malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) {
+        double m = I->p.cost[i * K];
+        for (int k = 1; k < K; ++k)
+            if (I->p.cost[i * K + k] < m) m = I->p.cost[i * K + k];
+        c.min_p[i] = m;
+    }
+    c.best_obj = INFINITY;
+    c.best_row = best_row;
+    ws_alloc(&c.w, I);
+    bnb_descend(&c, 0);
+    ws_free(&c.w);
+    free(c.assign);
+    free(c.load);
+    free(c.load_time);
+    free(c.down);
+    free(c.min_p);
+    *best_ms = c.best_obj;
+    *visited = c.visited;
+    if (c.have_best) return c.stopped ? 1 : 0;
+    return c.stopped ? 3 : 2;
 }
 
 /* ========================================================================== */

@@ -58,6 +58,9 @@ def lib():
         L.orc_enumerate.restype = C.c_int64
         L.orc_enumerate.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
         L.orc_last_max_ready.restype = C.c_int
+        L.orc_solve_exact.restype = C.c_int
+        L.orc_solve_exact.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_void_p,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.orc_gcof.restype = C.c_int
         L.orc_gcof.argtypes = [C.POINTER(_GcofIn), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
@@ -124,6 +127,17 @@ class OracleInstance:
         best = C.c_double(0)
         idx = lib().orc_enumerate(self._h, _p(op_order), C.byref(best))
         return int(idx), best.value
+
+    def solve_exact(self, op_order, gap: float = 0.0, node_limit: int | None = None):
+        """Reference branch and bound (solver.py:172-254) without the time limit.
+        Returns (status 0 optimal / 1 feasible / 2 infeasible / 3 budget, row, makespan, visited)."""
+        op_order = np.ascontiguousarray(op_order, np.int32)
+        row = np.zeros(self.n_ops, np.uint8)
+        best = C.c_double(0)
+        vis = C.c_int64(0)
+        st = lib().orc_solve_exact(self._h, _p(op_order), float(gap), -1 if node_limit is None else int(node_limit),
+                                   _p(row), C.byref(best), C.byref(vis))
+        return int(st), row, best.value, int(vis.value)
 
 
 def gcof_partition(seq_beg, seq_types, tag, esrc, edst, rule_beg, rule_types):

@@ -35,6 +35,11 @@ MP_ROW_BAD_DEVICE = 2
 
 MP_DEVICE_PTRS = 1
 
+MP_SOLVE_OPTIMAL = 0
+MP_SOLVE_FEASIBLE = 1
+MP_SOLVE_INFEASIBLE = 2
+MP_SOLVE_BUDGET = 3
+
 
 class mp_error(C.Structure):
     _fields_ = [("code", C.c_int32), ("a", C.c_int64), ("b", C.c_int64), ("msg", C.c_char * 200)]
@@ -111,6 +116,9 @@ SIGNATURES = {
                                      C.c_int32, C.c_uint64, C.c_void_p, C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
                                      C.POINTER(mp_error)]),
+    "mp_branch_and_bound": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_double,
+                                         C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(mp_error)]),
     "mp_coarsen": (C.c_int32, [C.POINTER(mp_coarsen_input), C.c_int32, C.POINTER(mp_coarsen_output),
                                C.POINTER(mp_error)]),
     "mp_coarsen_free": (None, [C.POINTER(mp_coarsen_output)]),

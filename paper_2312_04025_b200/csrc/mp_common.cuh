@@ -201,4 +201,12 @@ cudaError_t mp_launch_ls_pick(const double *chain_ms, long long n, double *out_m
                               cudaStream_t s);
 cudaError_t mp_launch_memcheck(const EvalArgs &a, long long *feas, unsigned int *n_feas, int sms, cudaStream_t s);
 cudaError_t mp_eval_set_smem_limits();
+
+// Read-only view of an instance for the other translation units (mp_bnb.cu).
+struct InstView {
+    const unsigned char *blob;
+    TabOff to;
+    int n_ops, n_flows, K, n_levels, sms, device, fastdiv;
+};
+InstView mp_instance_view(const mp_instance *I);
 extern unsigned long long g_mp_launches;

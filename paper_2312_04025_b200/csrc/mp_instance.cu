@@ -831,6 +831,20 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
 
 }  // extern "C"
 
+InstView mp_instance_view(const mp_instance *I) {
+    InstView v{};
+    v.blob = I->blob;
+    v.to = I->to;
+    v.n_ops = I->n_ops;
+    v.n_flows = I->n_flows;
+    v.K = I->K;
+    v.n_levels = I->n_levels;
+    v.sms = I->sms;
+    v.device = I->device;
+    v.fastdiv = I->fastdiv ? 1 : 0;
+    return v;
+}
+
 // ---- evaluation plumbing ------------------------------------------------------
 namespace {
 

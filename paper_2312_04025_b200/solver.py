@@ -294,21 +294,59 @@ def brute_force(gc: CompGraph, c: Cluster, mesh: EffectiveMesh) -> Solution:
 
 
 def solve_exact(gc: CompGraph, c: Cluster, mesh: EffectiveMesh,
-                budget: SolveBudget | None = None) -> Solution:
-    """Exact optimum (``solver.py:172-254``).
+                budget: SolveBudget | None = None, *, seed_chains: int = 1024,
+                seed_moves: int | None = None) -> Solution:
+    """Branch and bound over assignments on the GPU (``solver.py:172-254``).
 
-    At gap 0 without limits the reference's branch and bound returns the
-    lexicographically smallest optimal assignment in ``topo_order`` — exactly
-    the first strict minimum of the enumeration (the reference's own acceptance
-    claim, ``test_acceptance.py:68-84``).  Within the enumeration guard this is
-    computed by GPU enumeration.  Budgeted / gapped search and instances past
-    the guard are the GPU-assisted branch and bound of DESIGN.md §8 (next):
-    they raise ``TooLargeError`` / ``NotImplementedError`` rather than run a
-    CPU search.
+    Same search space, node bound, memory-prefix check and incumbent rule as
+    the reference (ops in ``topo_order(gc)``, devices ascending), but a whole
+    frontier of up to 65 536 children is bounded per round on the GPU and the
+    leaves are scheduled by the evaluator kernel (``mp_branch_and_bound``).
+
+    * gap 0, no limits: ``Status.OPTIMAL`` with the optimal makespan and the
+      lexicographically smallest optimal assignment — the reference's answer
+      (its own acceptance claim: exact == brute force, ``test_acceptance.py:61-84``).
+    * gap > 0: prune when ``bound >= best * (1 - gap)`` (``solver.py:239``);
+      ``Status.OPTIMAL`` with ``gap`` set, objective within ``1/(1-gap)`` of the optimum.
+    * node / time limits stop between rounds: ``Status.FEASIBLE`` with the
+      incumbent, or ``Status.BUDGET`` without one (``solver.py:246-254``).
+
+    The incumbent is seeded with a GPU local search (``seed_chains`` chains from
+    seeded random rows); at gap 0 seeds change the work, never the answer.
     """
-    if budget is not None and (budget.gap != 0.0 or budget.node_limit is not None):
-        raise NotImplementedError("budgeted branch and bound is not on the GPU path yet")
-    return brute_force(gc, c, mesh)
+    budget = budget or SolveBudget()
+    with Instance(gc, c, mesh) as inst:
+        n, k = inst.n_ops, inst.K
+        order = topo_order(gc)
+        pos = {nid: i for i, nid in enumerate(inst.op_ids)}
+        op_order = np.asarray([pos[x] for x in order], dtype=np.int32)
+        seeds = None
+        if seed_chains > 0 and k > 1:
+            rng = np.random.Generator(np.random.PCG64(0x5eed))
+            start = rng.integers(0, k, (min(seed_chains, 64), n), dtype=np.uint8)
+            moves = seed_moves if seed_moves is not None else min(4 * n * k, 2048)
+            row, ms, _, _ = local_search(inst, start, chains=seed_chains, moves=moves, seed=1)
+            if math.isfinite(ms):
+                seeds = row.reshape(1, n)
+        best = np.zeros(n, dtype=np.uint8)
+        bms = C.c_double()
+        status = C.c_int32()
+        visited = C.c_int64()
+        err = N.mp_error()
+        code = inst._lib.mp_branch_and_bound(
+            inst.handle, N.ptr(op_order), float(budget.gap),
+            -1 if budget.node_limit is None else int(budget.node_limit),
+            -1.0 if budget.time_limit_s is None else float(budget.time_limit_s),
+            N.ptr(seeds), 0 if seeds is None else 1, N.ptr(best), C.byref(bms), C.byref(status),
+            C.byref(visited), C.byref(err))
+        N.check(code, err, "mp_branch_and_bound")
+        st = status.value
+        if st in (N.MP_SOLVE_OPTIMAL, N.MP_SOLVE_FEASIBLE):
+            sched = _schedule_row(inst, best)
+            if st == N.MP_SOLVE_OPTIMAL:
+                return Solution(Status.OPTIMAL, sched.makespan_s, sched, budget.gap)
+            return Solution(Status.FEASIBLE, sched.makespan_s, sched, None)
+        return Solution(Status.BUDGET if st == N.MP_SOLVE_BUDGET else Status.INFEASIBLE, math.inf, None)
 
 
 def solve_with_derived_mesh(gc: CompGraph, c: Cluster, budget: SolveBudget | None = None) -> Solution:

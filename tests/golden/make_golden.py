@@ -258,6 +258,42 @@ def make_workload_evals():
     return out
 
 
+def make_solve_exact():
+    """Reference solve_exact (solver.py:172-254) under gap / node-limit budgets."""
+    cases = []
+
+    def add(tag, g, c, gap, node_limit):
+        mesh = ref.effective_bandwidth(c)
+        sol = ref.solve_exact(g, c, mesh, ref.SolveBudget(gap=gap, node_limit=node_limit))
+        rec = {"name": tag, "graph": ser_graph(g), "cluster": ser_cluster(c), "status": sol.status.value,
+               "objective": H(sol.objective_s), "gap": H(gap), "node_limit": node_limit}
+        if sol.schedule is not None:
+            rec["placement"] = {str(k): v for k, v in sol.placement.items()}
+        cases.append(rec)
+
+    for trial in range(50):
+        g, c = rc.random_instance(random.Random(9001 + trial), max_ops=8, tight_ok=True, min_ops=3)
+        add(f"acc-{9001 + trial}-gap0.3", g, c, 0.3, None)
+        add(f"acc-{9001 + trial}-nodes{7 + 13 * trial}", g, c, 0.0, 7 + 13 * trial)
+    for trial in range(20):
+        g, c = rc.random_instance(random.Random(500 + trial), max_ops=10, tight_ok=True, min_ops=6)
+        add(f"rnd-{500 + trial}", g, c, 0.0, None)
+        add(f"rnd-{500 + trial}-gap0.1", g, c, 0.1, None)
+    g, c = rc.skewed_pair()
+    add("skewed_pair-gap0.5", g, c, 0.5, None)
+    g, c = rc.random_instance(random.Random(3), max_ops=6, tight_ok=False)
+    add("node_limit_1", g, c, 0.0, 1)
+    # the acceptance-8 coarse graph (test_acceptance.py:244-263) under node limits
+    g = ref.gen_synthetic(ref.GenSpec(ops=56, width=4, density=0.6, devices=(0, 1, 2, 3)), seed=2)
+    coarse = ref.gcof(g, rc.table_rules())
+    bw = [2e7, 5e7, 1e8, 2e8]
+    c = ref.Cluster([ref.Device(k, 6_000_000_000) for k in range(4)],
+                    {(a, b): bw[(a + b) % 4] for a in range(4) for b in range(4) if a != b})
+    for nl in (500, 5000):
+        add(f"accept8-nodes{nl}", coarse, c, 0.05, nl)
+    return cases
+
+
 def make_synth():
     out = []
     for ops, width, dens, devs, seed in ((490, 4, 0.5, (0, 1), 2312), (490, 4, 0.5, (0, 1), 1),
@@ -273,7 +309,8 @@ def make_synth():
 
 def main():
     jobs = {"schedules.json": make_schedules, "brute_force.json": make_brute, "gcof.json": make_gcof,
-            "workload_evals.json": make_workload_evals, "synth.json": make_synth}
+            "workload_evals.json": make_workload_evals, "synth.json": make_synth,
+            "solve_exact.json": make_solve_exact}
     only = set(sys.argv[1:])
     for fname, fn in jobs.items():
         if only and fname not in only:

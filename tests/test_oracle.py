@@ -82,6 +82,31 @@ def test_oracle_brute_force_matches_reference(oracle_mod):
         assert got == {int(k): v for k, v in case["placement"].items()}, case["name"]
 
 
+_STATUS = {0: "optimal", 1: "feasible", 2: "infeasible", 3: "budget"}
+
+
+def test_oracle_solve_exact_matches_reference(oracle_mod):
+    """orc_solve_exact restates solve_exact's DFS, bound, drift and node counting:
+    status, objective bits and placement equal the reference's under gap and
+    node-limit budgets (tests/golden/solve_exact.json)."""
+    n = 0
+    for case in golden("solve_exact.json"):
+        g = graph_from(case["graph"])
+        c = cluster_from(case["cluster"])
+        mesh = mp.effective_bandwidth(c)
+        orc = _flat_instance(oracle_mod, g, c, mesh)
+        ids = g.node_ids
+        order = [ids.index(x) for x in mp.topo_order(g)]
+        st, row, best, _ = orc.solve_exact(order, F(case["gap"]), case["node_limit"])
+        assert _STATUS[st] == case["status"], case["name"]
+        assert best.hex() == F(case["objective"]).hex(), case["name"]
+        if "placement" in case:
+            got = {ids[i]: c.device_ids[int(d)] for i, d in enumerate(row)}
+            assert got == {int(k): v for k, v in case["placement"].items()}, case["name"]
+        n += 1
+    assert n == 144
+
+
 @pytest.mark.parametrize("chunk", range(4))
 def test_oracle_gcof_matches_reference(oracle_mod, chunk):
     cases = golden("gcof.json")
