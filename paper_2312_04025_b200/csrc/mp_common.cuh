@@ -98,6 +98,7 @@ struct EvalArgs {
     int want_argmin;
     int row_list;                 // 1: `row_idx` lists the global rows to (re)evaluate
     const long long *row_idx;     // [n_rows] global row indices (row_list mode)
+    long long lane_stride;        // TPP: lanes in the grid (stride of the lane-interleaved global state)
 };
 
 enum { SRC_LOAD = 0, SRC_ENUM = 1 };
@@ -201,6 +202,11 @@ cudaError_t mp_launch_ls_pick(const double *chain_ms, long long n, double *out_m
                               cudaStream_t s);
 cudaError_t mp_launch_memcheck(const EvalArgs &a, long long *feas, unsigned int *n_feas, int sms, cudaStream_t s);
 cudaError_t mp_eval_set_smem_limits();
+// Thread-per-placement evaluator (mp_eval.cu mp_tpp_kernel): `rc` ready entries
+// held in registers (4, 8 or 16), `threads` placements per CTA.
+#define MP_TPP_MAX_THREADS 512
+cudaError_t mp_launch_tpp(int rc, int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s);
+size_t mp_tpp_state_bytes(int n_ops, int n_multi, long long lanes);
 
 // Read-only view of an instance for the other translation units (mp_bnb.cu).
 struct InstView {

@@ -697,6 +697,316 @@ __global__ void mp_ls_pick_kernel(const double *chain_ms, long long n, double *o
     }
 }
 
+// ---- K3/K4, thread-per-placement variant (TPP) ---------------------------------------
+// One LANE evaluates one placement; the 32 placements of a warp advance in
+// lockstep through the same instruction stream.  Chosen when the calibrated ready
+// set is small (<= 16 entries), which is the case for the layered model graphs
+// (C2-C4):
+//   * the ready set lives in REGISTERS: RC entries {est, rank, dur, meta, tie},
+//     fully unrolled, with a validity bitmask — removal clears a bit, insertion
+//     fills the first free slot;
+//   * the placement row and the 3K+2 resource clocks live in shared memory,
+//     lane-interleaved ([index][lane]: conflict-free, the row read for a common op
+//     is one wavefront); the instance tables are staged by TMA as in the group
+//     kernel;
+//   * ranks and the multi-input op state live in global memory, lane-interleaved
+//     ([op][lane]), so the rank pass — every lane walks the ops in the same
+//     height order — reads and writes them fully coalesced.
+// Semantics are those of eval_lockstep (same keys, same co-located-flow gate ids);
+// rows whose ready set outgrows RC are re-run by the off-chip group variant.
+size_t tpp_state_bytes(int n_ops, int n_multi, long long L) {
+    return static_cast<size_t>(L) * (8ULL * n_ops + 16ULL * n_multi) + 64;
+}
+
+template <int RC, bool COLO>
+__global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __grid_constant__ EvalArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ double s_best_ms[MP_TPP_MAX_THREADS / 32];
+    __shared__ long long s_best_row[MP_TPP_MAX_THREADS / 32];
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int n_ops = a.n_ops, K = a.K;
+    stage_tables(sm, a, &s_bar);
+    const unsigned char *tb = sm;
+    unsigned char *rowt = sm + a.to.bytes;  // [n_ops][T]
+    double *clk = reinterpret_cast<double *>(sm + a.to.bytes + ((static_cast<size_t>(n_ops) * T + 15) & ~static_cast<size_t>(15)));
+    unsigned long long *ld = reinterpret_cast<unsigned long long *>(clk);  // memory loads alias the clocks
+    const long long L = a.lane_stride;
+    const long long gl = static_cast<long long>(blockIdx.x) * T + tid;
+    double *g_rank = reinterpret_cast<double *>(a.gstate) + gl;
+    double *g_mest = reinterpret_cast<double *>(a.gstate) + static_cast<long long>(n_ops) * L + gl;
+    uint32_t *g_mtie = reinterpret_cast<uint32_t *>(reinterpret_cast<double *>(a.gstate) +
+                                                    static_cast<long long>(n_ops + a.n_multi) * L) + gl;
+    uint32_t *g_mnp = g_mtie + static_cast<long long>(a.n_multi) * L;
+
+    const double *__restrict__ T_cost = tab<double>(tb, a.to.cost);
+    const long long *__restrict__ T_mem = tab<long long>(tb, a.to.mem);
+    const long long *__restrict__ T_cap = tab<long long>(tb, a.to.cap);
+    const double *__restrict__ T_bw = tab<double>(tb, a.to.bw);
+    const double *__restrict__ T_rbw = tab<double>(tb, a.to.rbw);
+    const double2 *__restrict__ T_rec = tab<double2>(tb, a.to.s_rec);
+    const uint32_t *__restrict__ T_out_beg = tab<uint32_t>(tb, a.to.out_beg);
+    const uint32_t *__restrict__ T_fdst = tab<uint32_t>(tb, a.to.fdst);
+    const uint32_t *__restrict__ T_mi = tab<uint32_t>(tb, a.to.mi);
+    const uint32_t *__restrict__ T_lvl = tab<uint32_t>(tb, a.to.lvl_ops);
+    const uint32_t *__restrict__ T_srcs = tab<uint32_t>(tb, a.to.srcs);
+    const uint32_t *__restrict__ T_mdeg = tab<uint32_t>(tb, a.to.m_deg);
+    const uint32_t *__restrict__ T_mop = tab<uint32_t>(tb, a.to.m_op);
+    const int fast = a.fastdiv;
+    const uint32_t RZ = static_cast<uint32_t>(3 * K);
+    const uint32_t WS = RZ + 1;
+    const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
+    double best_ms = kInf;
+    long long best_row = LLONG_MAX;
+    constexpr unsigned FULLRC = (RC >= 32) ? 0xffffffffu : ((1u << RC) - 1u);
+
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next, 32ULL);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= static_cast<unsigned long long>(n_rows)) break;
+        const unsigned long long p = base + lane;
+        const bool live = p < static_cast<unsigned long long>(n_rows);
+        const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
+        const long long grow = a.row_base + lrow;
+
+        // ---- the row -> shared memory column `tid` ------------------------------------
+        bool bad = false;
+        {
+            const long long start = lrow * n_ops;
+            const long long a0 = start & ~15LL;
+            const long long a1 = (start + n_ops + 15) & ~15LL;
+            const int chunks = live ? static_cast<int>((a1 - a0) >> 4) : 0;
+            for (int c = 0; c < chunks; ++c) {
+                const long long off = a0 + 16LL * c;
+                uint4 v;
+                if (off + 16 <= a.rows_bytes) {
+                    v = __ldcs(reinterpret_cast<const uint4 *>(a.rows + off));
+                } else {
+                    uint32_t w[4] = {0, 0, 0, 0};
+                    for (int b = 0; b < 16; ++b)
+                        if (off + b < a.rows_bytes) w[b >> 2] |= static_cast<uint32_t>(a.rows[off + b]) << (8 * (b & 3));
+                    v = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int b = 0; b < 16; ++b) {
+                    const long long pos = off + b - start;
+                    if (pos >= 0 && pos < n_ops) {
+                        const unsigned char d = static_cast<unsigned char>(w4[b >> 2] >> (8 * (b & 3)));
+                        bad |= d >= K;
+                        rowt[pos * T + tid] = d;
+                    }
+                }
+            }
+            if (!live || bad) {
+                for (int i = 0; i < n_ops; ++i) rowt[i * T + tid] = 0;  // keep the lockstep passes in bounds
+            }
+        }
+        // ---- 1. memory feasibility (solver.py:82-87) ------------------------------------
+        int status = bad ? MP_ROW_BAD_DEVICE : MP_ROW_OK;
+        int over_dev = -1;
+        long long over_by = 0;
+        for (int k = 0; k < K; ++k) ld[k * T + tid] = 0ULL;
+        if (live && !bad) {
+            for (int i = 0; i < n_ops; ++i) {
+                const int d = rowt[i * T + tid];
+                ld[d * T + tid] += static_cast<unsigned long long>(T_mem[i]);
+            }
+            for (int k = 0; k < K; ++k) {
+                const long long l = static_cast<long long>(ld[k * T + tid]);
+                if (l > T_cap[k]) {
+                    status = MP_ROW_MEMORY;
+                    over_dev = k;
+                    over_by = l - T_cap[k];
+                    break;
+                }
+            }
+        }
+        const bool alive = live && status == MP_ROW_OK;
+
+        // ---- 2+3. durations + rank, ops in ascending height (solver.py:89-107) -----------
+        for (int t = 0; t < n_ops; ++t) {
+            const int i = static_cast<int>(T_lvl[t]);
+            const int d = rowt[i * T + tid];
+            double best = 0.0;
+            const int qe = static_cast<int>(T_out_beg[i + 1]);
+            for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
+                const double2 rec = T_rec[q];
+                const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+                const int dj = rowt[j * T + tid];
+                const bool cross = dj != d;
+                const int bi = cross ? d * K + dj : 0;
+                const double dv = div_bw(rec.y, cross ? T_bw[bi] : 1.0, cross ? T_rbw[bi] : 1.0, fast);
+                const double rj = g_rank[static_cast<long long>(j) * L];
+                const double fr = cross ? dv + rj : rj;
+                best = fr > best ? fr : best;
+            }
+            g_rank[static_cast<long long>(i) * L] = T_cost[i * K + d] + best;
+        }
+
+        // ---- 4. dispatch state (solver.py:109-116) -----------------------------------------
+        for (int k = 0; k < a.n_multi; ++k) {
+            g_mnp[static_cast<long long>(k) * L] = T_mdeg[k];
+            g_mest[static_cast<long long>(k) * L] = 0.0;
+            g_mtie[static_cast<long long>(k) * L] = T_mop[k];
+        }
+        for (int k = 0; k <= static_cast<int>(WS); ++k) clk[k * T + tid] = 0.0;
+        unsigned long long E[RC], R[RC];
+        double D[RC];
+        uint32_t M[RC], TI[RC];
+#pragma unroll
+        for (int s = 0; s < RC; ++s) {
+            E[s] = 0ULL;
+            R[s] = 0ULL;
+            D[s] = 0.0;
+            M[s] = (RZ << 20) | (RZ << 26);
+            TI[s] = 0u;
+        }
+        unsigned validm = 0u;
+        bool ovf = false;
+        auto insert = [&](unsigned long long est, unsigned long long rk, double du, uint32_t meta, uint32_t tie) {
+            const unsigned fr = ~validm & FULLRC;
+            if (fr == 0u) {
+                ovf = true;
+                return;
+            }
+            const int sf = __ffs(fr) - 1;
+#pragma unroll
+            for (int s = 0; s < RC; ++s) {
+                if (s == sf) {
+                    E[s] = est;
+                    R[s] = rk;
+                    D[s] = du;
+                    M[s] = meta;
+                    TI[s] = tie;
+                }
+            }
+            validm |= 1u << sf;
+        };
+        if (alive) {
+            for (int t = 0; t < a.n_src; ++t) {
+                const int i = static_cast<int>(T_srcs[t]);
+                const int d = rowt[i * T + tid];
+                insert(0ULL, dbits(g_rank[static_cast<long long>(i) * L]), T_cost[i * K + d],
+                       static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26),
+                       static_cast<uint32_t>(i));
+            }
+        }
+        bool done = !alive || ovf;
+        double ms = 0.0;
+        while (__any_sync(kFull, !done)) {
+            const int hb = done ? 0 : 32 - __clz(validm);
+            const int hbw = __reduce_max_sync(kFull, hb);
+            if (!done) {
+                // -- scan the ready entries for the minimum (e, -rank, id) key -------------
+                unsigned long long be = ~0ULL, br = 0ULL;
+                uint32_t bi = 0xffffffffu, bm = 0u;
+                double bd = 0.0;
+                int bs = 0;
+#pragma unroll
+                for (int s = 0; s < RC; ++s) {
+                    if (s >= hbw) break;
+                    const uint32_t m = M[s];
+                    const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
+                    const unsigned long long c1 = dbits(clk[(i1 <= WS ? i1 : RZ) * T + tid]);
+                    const unsigned long long c2 = dbits(clk[(i2 <= WS ? i2 : RZ) * T + tid]);
+                    unsigned long long e = E[s] > c1 ? E[s] : c1;
+                    e = e > c2 ? e : c2;
+                    const uint32_t id = (COLO && e == E[s]) ? TI[s] : (m & MP_NODE_MASK);
+                    const bool take = ((validm >> s) & 1u) && key_less_nb(e, R[s], id, be, br, bi);
+                    be = take ? e : be;
+                    br = take ? R[s] : br;
+                    bi = take ? id : bi;
+                    bm = take ? m : bm;
+                    bd = take ? D[s] : bd;
+                    bs = take ? s : bs;
+                }
+                validm &= ~(1u << bs);
+                // -- commit (solver.py:130-138) ------------------------------------------------
+                const double end = bitsd(be) + bd;
+                const int node = static_cast<int>(bm & MP_NODE_MASK);
+                const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+                clk[(r1 == RZ ? WS : r1) * T + tid] = end;
+                clk[(r2 == RZ ? WS : r2) * T + tid] = end;
+                const bool isop = node < n_ops;
+                ms = (isop && end > ms) ? end : ms;
+                // -- successors (solver.py:140-145) ------------------------------------------
+                auto op_update = [&](int j, int dj, bool via_colo, uint32_t pid) {
+                    const uint32_t k = T_mi[j];
+                    const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+                    const uint32_t meta = static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26);
+                    if (k != MP_NONE) {
+                        const long long o = static_cast<long long>(k) * L;
+                        const uint32_t np = g_mnp[o] - 1u;
+                        const double cur = g_mest[o];
+                        const uint32_t ct = g_mtie[o];
+                        const bool up = end > cur;
+                        const double ej = up ? end : cur;
+                        const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
+                        g_mnp[o] = np;
+                        g_mest[o] = ej;
+                        g_mtie[o] = tie_new;
+                        if (np == 0u)
+                            insert(dbits(ej), dbits(g_rank[static_cast<long long>(j) * L]), T_cost[j * K + dj], meta,
+                                   tie_new);
+                    } else {
+                        insert(dbits(end), dbits(g_rank[static_cast<long long>(j) * L]), T_cost[j * K + dj], meta, tj);
+                    }
+                };
+                if (isop) {
+                    const int d = static_cast<int>(r1);
+                    const int qe = static_cast<int>(T_out_beg[node + 1]);
+                    for (int q = static_cast<int>(T_out_beg[node]); q < qe; ++q) {
+                        const double2 rec = T_rec[q];
+                        const unsigned long long rb = dbits(rec.x);
+                        const int j = static_cast<int>(static_cast<uint32_t>(rb));
+                        const uint32_t pid = static_cast<uint32_t>(rb >> 32);
+                        const int dj = rowt[j * T + tid];
+                        const bool cross = dj != d;
+                        if (COLO && !cross) {
+                            op_update(j, dj, true, pid);
+                        } else {
+                            const double fdur = cross ? div_bw(rec.y, T_bw[d * K + dj], T_rbw[d * K + dj], fast) : 0.0;
+                            const double rj = g_rank[static_cast<long long>(j) * L];
+                            const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                                   (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                                : ((RZ << 20) | (RZ << 26)));
+                            insert(dbits(end), dbits(fdur + rj), fdur, fmeta, pid);
+                        }
+                    }
+                } else {
+                    const int j = static_cast<int>(T_fdst[node - n_ops]);
+                    op_update(j, rowt[j * T + tid], false, static_cast<uint32_t>(node));
+                }
+                done = ovf || validm == 0u;
+            }
+        }
+        if (live) {
+            const long long o = grow - a.out_base;
+            if (ovf) {
+                const unsigned int k = atomicAdd(a.ovf_count, 1u);
+                a.ovf_rows[k] = grow;
+                if (a.status) a.status[o] = MP_ROW_OVERFLOW;
+            } else {
+                const double r = alive ? ms : kInf;
+                if (a.makespan) a.makespan[o] = r;
+                if (a.status) a.status[o] = static_cast<int8_t>(status);
+                if (a.mem_dev) a.mem_dev[o] = over_dev;
+                if (a.overflow) a.overflow[o] = over_by;
+                if (alive && (r < best_ms || (r == best_ms && grow < best_row))) {
+                    best_ms = r;
+                    best_row = grow;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (a.want_argmin) cta_keep_best(a, best_ms, best_row, s_best_ms, s_best_row);
+}
+
 // ---- host launch table -----------------------------------------------------------------
 namespace {
 typedef void (*EvalFn)(const EvalArgs);
@@ -840,6 +1150,29 @@ cudaError_t mp_launch_eval(const LaunchShape &ls, int src_mode, bool trace, cons
     const int mode = trace ? 0 : ls.mode;
     EvalFn f = pick_any(ls.G, src_mode, mode, trace, a.colo != 0);
     f<<<ls.ctas, ls.threads, mode ? ls.smem : 0, s>>>(a);
+    ++g_mp_launches;
+    return cudaGetLastError();
+}
+
+size_t mp_tpp_state_bytes(int n_ops, int n_multi, long long lanes) { return tpp_state_bytes(n_ops, n_multi, lanes); }
+
+cudaError_t mp_launch_tpp(int rc, int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s) {
+    static bool attr = false;
+    EvalFn f4 = a.colo ? mp_tpp_kernel<4, true> : mp_tpp_kernel<4, false>;
+    EvalFn f8 = a.colo ? mp_tpp_kernel<8, true> : mp_tpp_kernel<8, false>;
+    EvalFn f16 = a.colo ? mp_tpp_kernel<16, true> : mp_tpp_kernel<16, false>;
+    if (!attr) {
+        const EvalFn all[6] = {mp_tpp_kernel<4, true>, mp_tpp_kernel<4, false>, mp_tpp_kernel<8, true>,
+                               mp_tpp_kernel<8, false>, mp_tpp_kernel<16, true>, mp_tpp_kernel<16, false>};
+        for (EvalFn f : all) {
+            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    EvalFn f = rc <= 4 ? f4 : (rc <= 8 ? f8 : f16);
+    f<<<ctas, threads, smem, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
 }

@@ -337,6 +337,10 @@ struct mp_instance {
     LaunchShape wide{};
     StOff wide_so{};
     DevBuf main_state, wide_state;
+    // thread-per-placement variant (mp_tpp_kernel); tpp_rc == 0: not used
+    bool tpp_allowed = true;
+    int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
+    DevBuf tpp_state;
     // per-call scratch
     DevBuf ctrs;      // [0] main next, [1] wide next, [2] ovf count (u32) ...
     DevBuf cta_best;  // ms[] then rows[]
@@ -443,7 +447,26 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
         I->main_so = so;
         I->main_rcap = rcap;
     }
+    // thread-per-placement variant: automatic shape, small calibrated ready set,
+    // instance tables + per-lane row and clocks in shared memory
+    I->tpp_rc = 0;
+    if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
+        const int rc = rcap <= 4 ? 4 : (rcap <= 8 ? 8 : (rcap <= 16 ? 16 : 0));
+        const long long per_lane = n_ops + 8LL * (3 * K + 2);
+        const long long avail = static_cast<long long>(smem_cap) - I->to.bytes - 32;
+        const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
+        if (rc > 0 && T >= 128) {
+            I->tpp_rc = rc;
+            I->tpp_threads = T;
+            I->tpp_ctas = std::min(I->sms, I->main.ctas);
+            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * T + 15) & ~15LL) +
+                                           8LL * (3 * K + 2) * T);
+        }
+    }
 }
+
+// ready capacity of the variant that runs first (rows beyond it re-run off-chip)
+int first_rcap(const mp_instance *I) { return I->tpp_rc > 0 ? I->tpp_rc : I->main_rcap; }
 
 EvalArgs base_args(const mp_instance *I, bool wide) {
     EvalArgs a{};
@@ -809,6 +832,8 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->fastdiv = I->fastdiv ? 1 : 0;
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
+    info->tpp_ready_cap = I->tpp_rc;
+    info->tpp_threads = I->tpp_rc > 0 ? I->tpp_threads : 0;
     return MP_OK;
 }
 
@@ -825,6 +850,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     std::lock_guard<std::mutex> lk(I->mu);
     I->rcap_target = ready_cap > 0 ? ready_cap : (I->peak_probe > 0 ? std::max(4, 2 * I->peak_probe) : 32);
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
+    I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm);
     return MP_OK;
 }
@@ -858,7 +884,11 @@ cudaError_t prepare(mp_instance *I, bool argmin, long long max_rows) {
     if ((e = I->ctrs.ensure(64)) != cudaSuccess) return e;
     const int nb = I->main.ctas + I->wide.ctas;
     if ((e = I->cta_best.ensure(static_cast<size_t>(nb) * 16 + 64)) != cudaSuccess) return e;
-    if (I->main_rcap < I->ready_bound) {
+    if (I->tpp_rc > 0) {
+        e = I->tpp_state.ensure(mp_tpp_state_bytes(I->n_ops, I->n_multi, static_cast<long long>(I->tpp_ctas) * I->tpp_threads));
+        if (e != cudaSuccess) return e;
+    }
+    if (first_rcap(I) < I->ready_bound) {
         e = I->wide_state.ensure(static_cast<size_t>(I->wide.ctas) * (I->wide.groups_per_cta + 1) * I->wide_so.bytes);
         if (e != cudaSuccess) return e;
         e = I->ovf_rows.ensure(static_cast<size_t>(std::max(1LL, max_rows)) * 8);
@@ -917,8 +947,14 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
         a.row_idx = static_cast<const long long *>(I->feas_rows.p);
         a.n_rows_dev = nf;
     }
-    if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) return e;
-    if (I->main_rcap < I->ready_bound) {
+    if (I->tpp_rc > 0) {
+        a.lane_stride = static_cast<long long>(I->tpp_ctas) * I->tpp_threads;
+        a.gstate = static_cast<unsigned char *>(I->tpp_state.p);
+        if ((e = mp_launch_tpp(I->tpp_rc, I->tpp_threads, I->tpp_ctas, I->tpp_smem, a, s)) != cudaSuccess) return e;
+    } else if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) {
+        return e;
+    }
+    if (first_rcap(I) < I->ready_bound) {
         // rows whose ready set outgrew the on-chip capacity: re-run off-chip
         EvalArgs b = base_args(I, true);
         b.rows = rows;

@@ -216,11 +216,15 @@ def random_problem(rng, n_ops, k, tight=False, ties=False, zero=False):
 SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (1, 2, 4, 8, 16, 32) for colo in (True, False)
           for rc in (0, 3)] + [dict(group_lanes=1, lanes_used=8), dict(group_lanes=2, lanes_used=16),
                                dict(group_lanes=4, lanes_used=8, ready_cap=2)]
+# automatic shape -> the thread-per-placement kernel when the calibrated ready set
+# fits its register capacity (4 / 8 / 16 entries; ready_cap=3 forces reruns)
+TPP_SHAPES = [dict(), dict(colo=False), dict(ready_cap=3), dict(ready_cap=6, colo=False), dict(ready_cap=12)]
 
 
 @pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
 def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
     rng = random.Random({"plain": 1, "tight": 2, "ties": 3, "zero": 4}[flavor])
+    tpp_runs = 0
     for trial in range(6):
         g, c = random_problem(rng, rng.randint(3, 60), rng.randint(2, 5), tight=flavor == "tight",
                               ties=flavor == "ties", zero=flavor == "zero")
@@ -230,8 +234,9 @@ def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
             want, wst = orc.eval_batch(rows)
             feas = np.where(wst == 0)[0]
             want_best = int(feas[np.argmin(want[feas])]) if len(feas) else -1
-            for shape in SHAPES:
+            for shape in SHAPES + TPP_SHAPES:
                 inst.tune(**shape)
+                tpp_runs += inst.info()["tpp_ready_cap"] > 0
                 ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
                 assert np.array_equal(st, wst), (flavor, trial, shape)
                 assert np.array_equal(bits(ms), bits(want)), (flavor, trial, shape, inst.info())
@@ -239,6 +244,7 @@ def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
                 assert best == want_best, (flavor, trial, shape)
             if flavor == "zero":
                 assert inst.info()["colo_ok"] in (0, 1)
+    assert tpp_runs >= 10, tpp_runs
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
@@ -250,7 +256,8 @@ def test_eval_vs_oracle_workloads(oracle_mod, name):
         orc = oracle_mod.OracleInstance.from_instance(inst)
         rows = workloads.placements(w.seed, 4096 if name != "c5" else 256, inst.n_ops, inst.K)
         want, wst = orc.eval_batch(rows, threads=8)
-        for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False)):
+        for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False),
+                      dict(ready_cap=3), dict(tpp=False)):
             inst.tune(**shape)
             ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
             assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)
