@@ -867,122 +867,131 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __g
         }
         unsigned validm = 0u;
         bool ovf = false;
-        auto insert = [&](unsigned long long est, unsigned long long rk, double du, uint32_t meta, uint32_t tie) {
+        // branch-free insertion into the first free register slot (predicated by `ins`)
+        auto insert = [&](bool ins, unsigned long long est, unsigned long long rk, double du, uint32_t meta,
+                          uint32_t tie) {
             const unsigned fr = ~validm & FULLRC;
-            if (fr == 0u) {
-                ovf = true;
-                return;
-            }
-            const int sf = __ffs(fr) - 1;
+            const int sf = fr ? __ffs(fr) - 1 : RC;
+            ovf = ovf || (ins && fr == 0u);
 #pragma unroll
             for (int s = 0; s < RC; ++s) {
-                if (s == sf) {
-                    E[s] = est;
-                    R[s] = rk;
-                    D[s] = du;
-                    M[s] = meta;
-                    TI[s] = tie;
-                }
+                const bool w = ins && s == sf;
+                E[s] = w ? est : E[s];
+                R[s] = w ? rk : R[s];
+                D[s] = w ? du : D[s];
+                M[s] = w ? meta : M[s];
+                TI[s] = w ? tie : TI[s];
             }
-            validm |= 1u << sf;
+            validm |= (ins && fr) ? (1u << sf) : 0u;
         };
         if (alive) {
             for (int t = 0; t < a.n_src; ++t) {
                 const int i = static_cast<int>(T_srcs[t]);
                 const int d = rowt[i * T + tid];
-                insert(0ULL, dbits(g_rank[static_cast<long long>(i) * L]), T_cost[i * K + d],
+                insert(true, 0ULL, dbits(g_rank[static_cast<long long>(i) * L]), T_cost[i * K + d],
                        static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26),
                        static_cast<uint32_t>(i));
             }
         }
         bool done = !alive || ovf;
         double ms = 0.0;
+        // Every lane runs the same instruction stream: warp-uniform trip counts,
+        // selects instead of branches, only the stores predicated (as eval_lockstep).
         while (__any_sync(kFull, !done)) {
             const int hb = done ? 0 : 32 - __clz(validm);
             const int hbw = __reduce_max_sync(kFull, hb);
-            if (!done) {
-                // -- scan the ready entries for the minimum (e, -rank, id) key -------------
-                unsigned long long be = ~0ULL, br = 0ULL;
-                uint32_t bi = 0xffffffffu, bm = 0u;
-                double bd = 0.0;
-                int bs = 0;
+            // -- scan the ready entries for the minimum (e, -rank, id) key -----------------
+            unsigned long long be = ~0ULL, br = 0ULL;
+            uint32_t bi = 0xffffffffu, bm = (RZ << 20) | (RZ << 26);
+            double bd = 0.0;
+            int bs = 0;
 #pragma unroll
-                for (int s = 0; s < RC; ++s) {
-                    if (s >= hbw) break;
-                    const uint32_t m = M[s];
-                    const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
-                    const unsigned long long c1 = dbits(clk[(i1 <= WS ? i1 : RZ) * T + tid]);
-                    const unsigned long long c2 = dbits(clk[(i2 <= WS ? i2 : RZ) * T + tid]);
-                    unsigned long long e = E[s] > c1 ? E[s] : c1;
-                    e = e > c2 ? e : c2;
-                    const uint32_t id = (COLO && e == E[s]) ? TI[s] : (m & MP_NODE_MASK);
-                    const bool take = ((validm >> s) & 1u) && key_less_nb(e, R[s], id, be, br, bi);
-                    be = take ? e : be;
-                    br = take ? R[s] : br;
-                    bi = take ? id : bi;
-                    bm = take ? m : bm;
-                    bd = take ? D[s] : bd;
-                    bs = take ? s : bs;
-                }
-                validm &= ~(1u << bs);
-                // -- commit (solver.py:130-138) ------------------------------------------------
-                const double end = bitsd(be) + bd;
-                const int node = static_cast<int>(bm & MP_NODE_MASK);
-                const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+            for (int s = 0; s < RC; ++s) {
+                if (s >= hbw) break;
+                const uint32_t m = M[s];
+                const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
+                const unsigned long long c1 = dbits(clk[i1 * T + tid]);
+                const unsigned long long c2 = dbits(clk[i2 * T + tid]);
+                unsigned long long e = E[s] > c1 ? E[s] : c1;
+                e = e > c2 ? e : c2;
+                const uint32_t id = (COLO && e == E[s]) ? TI[s] : (m & MP_NODE_MASK);
+                const bool take = !done && ((validm >> s) & 1u) && key_less_nb(e, R[s], id, be, br, bi);
+                be = take ? e : be;
+                br = take ? R[s] : br;
+                bi = take ? id : bi;
+                bm = take ? m : bm;
+                bd = take ? D[s] : bd;
+                bs = take ? s : bs;
+            }
+            validm = done ? validm : (validm & ~(1u << bs));
+            // -- commit (solver.py:130-138) ------------------------------------------------
+            const double end = bitsd(be) + bd;
+            const int node = static_cast<int>(bm & MP_NODE_MASK);
+            const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+            if (!done) {
                 clk[(r1 == RZ ? WS : r1) * T + tid] = end;
                 clk[(r2 == RZ ? WS : r2) * T + tid] = end;
-                const bool isop = node < n_ops;
-                ms = (isop && end > ms) ? end : ms;
-                // -- successors (solver.py:140-145) ------------------------------------------
-                auto op_update = [&](int j, int dj, bool via_colo, uint32_t pid) {
-                    const uint32_t k = T_mi[j];
-                    const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
-                    const uint32_t meta = static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26);
-                    if (k != MP_NONE) {
-                        const long long o = static_cast<long long>(k) * L;
-                        const uint32_t np = g_mnp[o] - 1u;
-                        const double cur = g_mest[o];
-                        const uint32_t ct = g_mtie[o];
-                        const bool up = end > cur;
-                        const double ej = up ? end : cur;
-                        const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
-                        g_mnp[o] = np;
-                        g_mest[o] = ej;
-                        g_mtie[o] = tie_new;
-                        if (np == 0u)
-                            insert(dbits(ej), dbits(g_rank[static_cast<long long>(j) * L]), T_cost[j * K + dj], meta,
-                                   tie_new);
-                    } else {
-                        insert(dbits(end), dbits(g_rank[static_cast<long long>(j) * L]), T_cost[j * K + dj], meta, tj);
-                    }
-                };
-                if (isop) {
-                    const int d = static_cast<int>(r1);
-                    const int qe = static_cast<int>(T_out_beg[node + 1]);
-                    for (int q = static_cast<int>(T_out_beg[node]); q < qe; ++q) {
-                        const double2 rec = T_rec[q];
-                        const unsigned long long rb = dbits(rec.x);
-                        const int j = static_cast<int>(static_cast<uint32_t>(rb));
-                        const uint32_t pid = static_cast<uint32_t>(rb >> 32);
-                        const int dj = rowt[j * T + tid];
-                        const bool cross = dj != d;
-                        if (COLO && !cross) {
-                            op_update(j, dj, true, pid);
-                        } else {
-                            const double fdur = cross ? div_bw(rec.y, T_bw[d * K + dj], T_rbw[d * K + dj], fast) : 0.0;
-                            const double rj = g_rank[static_cast<long long>(j) * L];
-                            const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
-                                                                   (static_cast<uint32_t>(2 * K + dj) << 26))
-                                                                : ((RZ << 20) | (RZ << 26)));
-                            insert(dbits(end), dbits(fdur + rj), fdur, fmeta, pid);
-                        }
-                    }
-                } else {
-                    const int j = static_cast<int>(T_fdst[node - n_ops]);
-                    op_update(j, rowt[j * T + tid], false, static_cast<uint32_t>(node));
-                }
-                done = ovf || validm == 0u;
             }
+            const bool isop = node < n_ops;
+            ms = (!done && isop && end > ms) ? end : ms;
+            // -- successors (solver.py:140-145), one uniform loop over the warp's
+            //    largest successor count: op -> its out-flows, flow -> its consumer ---------
+            const int d = static_cast<int>(r1);
+            const int nodec = done ? 0 : node;
+            const int ob = static_cast<int>(T_out_beg[isop ? nodec : 0]);
+            const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
+            const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
+            const int maxc = __reduce_max_sync(kFull, cnt);
+            for (int t = 0; t < maxc; ++t) {
+                const bool act = t < cnt;
+                const int q = (act && isop) ? ob + t : 0;
+                const double2 rec = T_rec[q];
+                const unsigned long long rb = dbits(rec.x);
+                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                const int dj = rowt[j * T + tid];
+                const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
+                const bool cross = dj != d;
+                const bool via_colo = COLO && isop && !cross;
+                const bool flow_ins = act && isop && !via_colo;  // a flow enters the ready set
+                const bool op_upd = act && !flow_ins;            // j's npred / est / gate change
+                const bool fcross = isop && cross;
+                const int bi2 = fcross ? d * K + dj : 0;
+                const double fdur = fcross ? div_bw(rec.y, T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                const double rj = g_rank[static_cast<long long>(j) * L];
+                const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                       (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                    : ((RZ << 20) | (RZ << 26)));
+                // multi-input ops keep npred / est / gate id
+                const uint32_t k = T_mi[j];
+                const bool multi = k != MP_NONE;
+                const bool mupd = op_upd && multi;
+                const long long mo = static_cast<long long>(multi ? k : 0) * L;
+                uint32_t np1 = 1u, ct = 0u;
+                double cur = 0.0;
+                if (mupd) {
+                    np1 = g_mnp[mo];
+                    cur = g_mest[mo];
+                    ct = g_mtie[mo];
+                }
+                const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+                const uint32_t np = np1 - 1u;
+                const bool up = end > cur;
+                const double ej = multi ? (up ? end : cur) : end;
+                const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
+                const uint32_t tie_j = multi ? tie_new : tj;
+                if (mupd) {
+                    g_mnp[mo] = np;
+                    g_mest[mo] = ej;
+                    g_mtie[mo] = tie_new;
+                }
+                const bool op_ins = op_upd && (!multi || np == 0u);
+                const double odur = T_cost[j * K + dj];
+                insert(flow_ins || op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
+                       flow_ins ? fdur : odur,
+                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                       flow_ins ? pid : tie_j);
+            }
+            done = done || ovf || validm == 0u;
         }
         if (live) {
             const long long o = grow - a.out_base;
