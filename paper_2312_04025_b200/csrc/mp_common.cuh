@@ -206,6 +206,8 @@ cudaError_t mp_eval_set_smem_limits();
 // held in registers (4, 8 or 16), `threads` placements per CTA.
 #define MP_TPP_MAX_THREADS 512
 cudaError_t mp_launch_tpp(int rc, int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s);
+cudaError_t mp_launch_tpp_ls(int rc, int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls,
+                             cudaStream_t s);
 size_t mp_tpp_state_bytes(int n_ops, int n_multi, long long lanes);
 
 // Read-only view of an instance for the other translation units (mp_bnb.cu).

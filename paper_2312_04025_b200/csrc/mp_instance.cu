@@ -355,7 +355,7 @@ struct mp_instance {
 
 namespace {
 
-void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
+void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, int ready_cap_req = 0) {
     const int n_ops = I->n_ops, K = I->K;
     const int smem_cap = MP_SMEM_DYN_MAX;
     // Ready sets are antichains of the augmented DAG, so a vertex-disjoint path
@@ -451,7 +451,11 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req) {
     // instance tables + per-lane row and clocks in shared memory
     I->tpp_rc = 0;
     if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
-        const int rc = rcap <= 4 ? 4 : (rcap <= 8 ? 8 : (rcap <= 16 ? 16 : 0));
+        // register capacity: the smallest template >= the calibrated peak (not 2x: a
+        // register slot costs a select per field on every insertion; rows that
+        // outgrow it are re-run exactly by the off-chip variant)
+        const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
+        const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
         const long long per_lane = n_ops + 8LL * (3 * K + 2);
         const long long avail = static_cast<long long>(smem_cap) - I->to.bytes - 32;
         const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
@@ -851,7 +855,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->rcap_target = ready_cap > 0 ? ready_cap : (I->peak_probe > 0 ? std::max(4, 2 * I->peak_probe) : 32);
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
-    choose_shapes(I, group_lanes, lanes_used, ctas_per_sm);
+    choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }
 
@@ -992,7 +996,17 @@ int evaluate_impl(mp_instance *I, const uint8_t *rows, long long n_rows, double 
     const long long row_bytes = I->n_ops;
     const bool devptr = (flags & MP_DEVICE_PTRS) != 0;
     // chunking bounds the overflow list and the staging buffers in host mode
-    const long long chunk = devptr ? std::max(1LL, n_rows) : std::max(1LL, std::min(n_rows, (256LL << 20) / row_bytes));
+    // host mode: equal chunks of <= 256 MiB (a short remainder chunk would pay a
+    // whole batch latency), at least two when the batch is large so the H2D copy of
+    // one chunk overlaps the evaluation of the other
+    long long chunk = std::max(1LL, n_rows);
+    if (!devptr) {
+        const long long max_chunk = std::max(1LL, (256LL << 20) / row_bytes);
+        long long nch = (n_rows + max_chunk - 1) / max_chunk;
+        if (nch < 2 && n_rows >= 16LL * I->sms * 512) nch = 2;
+        nch = std::max(1LL, nch);
+        chunk = std::max(1LL, (n_rows + nch - 1) / nch);
+    }
     MP_CUDA(prepare(I, argmin, chunk));
     const int nb = I->main.ctas + I->wide.ctas;
     if (argmin) {
@@ -1259,7 +1273,17 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     ls.rng_seed = rng_seed;
     ls.chain_rows = drows;
     ls.chain_ms = dms;
-    MP_CUDA(mp_launch_ls(use_wide ? I->wide : I->main, a, ls, s));
+    // thread-per-placement chains when the instance has a TPP shape and the group
+    // kernel's capacity fits a register template (same capacity -> same results)
+    const int ls_rc = I->main_rcap <= 4 ? 4 : (I->main_rcap <= 8 ? 8 : (I->main_rcap <= 16 ? 16 : 0));
+    if (I->tpp_rc > 0 && ls_rc > 0) {
+        MP_CUDA(I->tpp_state.ensure(mp_tpp_state_bytes(I->n_ops, I->n_multi, static_cast<long long>(I->tpp_ctas) * I->tpp_threads)));
+        a.lane_stride = static_cast<long long>(I->tpp_ctas) * I->tpp_threads;
+        a.gstate = static_cast<unsigned char *>(I->tpp_state.p);
+        MP_CUDA(mp_launch_tpp_ls(ls_rc, I->tpp_threads, I->tpp_ctas, I->tpp_smem, a, ls, s));
+    } else {
+        MP_CUDA(mp_launch_ls(use_wide ? I->wide : I->main, a, ls, s));
+    }
     MP_CUDA(mp_launch_ls_pick(dms, n_chains, dbest, dbc, s));
     double hms = 0;
     long long hc = -1;
