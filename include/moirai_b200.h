@@ -106,6 +106,7 @@ typedef struct mp_instance_info {
     int64_t state_bytes;        /* per-placement dynamic state                       */
     int32_t tpp_ready_cap;      /* >0: thread-per-placement kernel in use, register ready capacity */
     int32_t tpp_threads;        /* placements per CTA of the thread-per-placement kernel */
+    int32_t tpp_kind;           /* 1: ready set in registers, 2: in shared memory            */
 } mp_instance_info;
 
 /* ---- library ------------------------------------------------------------ */
@@ -125,6 +126,8 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
  * (MP_TUNE_NO_COLO) dispatches co-located flows as ordinary steps.  Results
  * never depend on these knobs. */
 #define MP_TUNE_NO_COLO 1
+#define MP_TUNE_TPP_SMEM 4  /* thread-per-placement with the ready set in shared memory even
+                               when it fits the register templates */
 #define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernel (it is used only
                                with automatic G/U and a calibrated ready set <= 16) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,

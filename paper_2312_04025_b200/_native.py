@@ -64,7 +64,7 @@ class mp_instance_info(C.Structure):
         ("peak_probe", C.c_int32), ("prefilter", C.c_int32), ("mode", C.c_int32),
         ("fastdiv", C.c_int32),
         ("table_bytes", C.c_int64), ("state_bytes", C.c_int64),
-        ("tpp_ready_cap", C.c_int32), ("tpp_threads", C.c_int32),
+        ("tpp_ready_cap", C.c_int32), ("tpp_threads", C.c_int32), ("tpp_kind", C.c_int32),
     ]
 
 

@@ -209,6 +209,9 @@ cudaError_t mp_launch_tpp(int rc, int threads, int ctas, int smem, const EvalArg
 cudaError_t mp_launch_tpp_ls(int rc, int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls,
                              cudaStream_t s);
 size_t mp_tpp_state_bytes(int n_ops, int n_multi, long long lanes);
+// ... with the ready set in shared memory: capacity a.rcap, layout after the clocks
+cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s);
+cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls, cudaStream_t s);
 
 // Read-only view of an instance for the other translation units (mp_bnb.cu).
 struct InstView {

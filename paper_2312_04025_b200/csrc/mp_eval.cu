@@ -734,6 +734,9 @@ struct TppView {
     const uint32_t *T_out_beg, *T_fdst, *T_mi, *T_lvl, *T_srcs, *T_mdeg, *T_mop;
     int fast;
     uint32_t RZ, WS;
+    // shared-memory ready set (tpps_eval): [cap][T] each, dense per lane
+    unsigned long long *rE, *rR, *rM;  // est bits, rank bits, meta | tie << 32
+    double *rD;                        // duration
 };
 
 __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm) {
@@ -769,6 +772,11 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.fast = a.fastdiv;
     v.RZ = static_cast<uint32_t>(3 * a.K);
     v.WS = v.RZ + 1;
+    const size_t rdy = static_cast<size_t>(a.rcap) * v.T;
+    v.rE = reinterpret_cast<unsigned long long *>(v.clk + static_cast<size_t>(3 * a.K + 2) * v.T);
+    v.rR = v.rE + rdy;
+    v.rM = v.rR + rdy;
+    v.rD = reinterpret_cast<double *>(v.rM + rdy);
     return v;
 }
 
@@ -1042,6 +1050,225 @@ __device__ __forceinline__ TppResult tpp_eval(const TppView &v, const EvalArgs &
     return r;
 }
 
+// As tpp_eval with the ready set in shared memory (lane-interleaved, dense
+// [0, nr)): insertion is four stores at index nr, removal moves the last entry
+// into the hole, the duration is read only for the winner.
+template <bool COLO>
+__device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs &a, bool live, bool bad, int cap) {
+    const int T = v.T, tid = v.tid, n_ops = v.n_ops, K = v.K;
+    unsigned char *rowt = v.rowt;
+    double *clk = v.clk;
+    unsigned long long *ld = v.ld;
+    const long long L = v.L;
+    double *g_rank = v.g_rank, *g_mest = v.g_mest;
+    uint32_t *g_mtie = v.g_mtie, *g_mnp = v.g_mnp;
+    const double *__restrict__ T_cost = v.T_cost;
+    const long long *__restrict__ T_mem = v.T_mem;
+    const long long *__restrict__ T_cap = v.T_cap;
+    const double *__restrict__ T_bw = v.T_bw;
+    const double *__restrict__ T_rbw = v.T_rbw;
+    const double2 *__restrict__ T_rec = v.T_rec;
+    const uint32_t *__restrict__ T_out_beg = v.T_out_beg;
+    const uint32_t *__restrict__ T_fdst = v.T_fdst;
+    const uint32_t *__restrict__ T_mi = v.T_mi;
+    const uint32_t *__restrict__ T_lvl = v.T_lvl;
+    const uint32_t *__restrict__ T_srcs = v.T_srcs;
+    const uint32_t *__restrict__ T_mdeg = v.T_mdeg;
+    const uint32_t *__restrict__ T_mop = v.T_mop;
+    const int fast = v.fast;
+    const uint32_t RZ = v.RZ, WS = v.WS;
+    unsigned long long *rE = v.rE, *rR = v.rR, *rM = v.rM;
+    double *rD = v.rD;
+    TppResult r;
+    // ---- 1. memory feasibility (solver.py:82-87) ------------------------------------
+    int status = bad ? MP_ROW_BAD_DEVICE : MP_ROW_OK;
+    int over_dev = -1;
+    long long over_by = 0;
+    for (int k = 0; k < K; ++k) ld[k * T + tid] = 0ULL;
+    if (live && !bad) {
+        for (int i = 0; i < n_ops; ++i) {
+            const int d = rowt[i * T + tid];
+            ld[d * T + tid] += static_cast<unsigned long long>(T_mem[i]);
+        }
+        for (int k = 0; k < K; ++k) {
+            const long long l = static_cast<long long>(ld[k * T + tid]);
+            if (l > T_cap[k]) {
+                status = MP_ROW_MEMORY;
+                over_dev = k;
+                over_by = l - T_cap[k];
+                break;
+            }
+        }
+    }
+    const bool alive = live && status == MP_ROW_OK;
+    r.alive = alive;
+
+    // ---- 2+3. durations + rank, ops in ascending height (solver.py:89-107) -----------
+    for (int t = 0; t < n_ops; ++t) {
+        const int i = static_cast<int>(T_lvl[t]);
+        const int d = rowt[i * T + tid];
+        double best = 0.0;
+        const int qe = static_cast<int>(T_out_beg[i + 1]);
+        for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
+            const double2 rec = T_rec[q];
+            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+            const int dj = rowt[j * T + tid];
+            const bool cross = dj != d;
+            const int bi = cross ? d * K + dj : 0;
+            const double dv = div_bw(rec.y, cross ? T_bw[bi] : 1.0, cross ? T_rbw[bi] : 1.0, fast);
+            const double rj = g_rank[static_cast<long long>(j) * L];
+            const double fr = cross ? dv + rj : rj;
+            best = fr > best ? fr : best;
+        }
+        g_rank[static_cast<long long>(i) * L] = T_cost[i * K + d] + best;
+    }
+
+    // ---- 4. dispatch state (solver.py:109-116) -----------------------------------------
+    for (int k = 0; k < a.n_multi; ++k) {
+        g_mnp[static_cast<long long>(k) * L] = T_mdeg[k];
+        g_mest[static_cast<long long>(k) * L] = 0.0;
+        g_mtie[static_cast<long long>(k) * L] = T_mop[k];
+    }
+    for (int k = 0; k <= static_cast<int>(WS); ++k) clk[k * T + tid] = 0.0;
+    int nr = 0;
+    bool ovf = false;
+    auto insert = [&](bool ins, unsigned long long est, unsigned long long rk, double du, uint32_t meta,
+                      uint32_t tie) {
+        const bool room = nr < cap;
+        ovf = ovf || (ins && !room);
+        if (ins && room) {
+            const int o = nr * T + tid;
+            rE[o] = est;
+            rR[o] = rk;
+            rD[o] = du;
+            rM[o] = static_cast<unsigned long long>(meta) | (static_cast<unsigned long long>(tie) << 32);
+        }
+        nr += (ins && room) ? 1 : 0;
+    };
+    if (alive) {
+        for (int t = 0; t < a.n_src; ++t) {
+            const int i = static_cast<int>(T_srcs[t]);
+            const int d = rowt[i * T + tid];
+            insert(true, 0ULL, dbits(g_rank[static_cast<long long>(i) * L]), T_cost[i * K + d],
+                   static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26), static_cast<uint32_t>(i));
+        }
+    }
+    bool done = !alive || ovf;
+    double ms = 0.0;
+    while (__any_sync(kFull, !done)) {
+        const int hbw = __reduce_max_sync(kFull, done ? 0 : nr);
+        // -- scan the ready entries for the minimum (e, -rank, id) key -----------------
+        unsigned long long be = ~0ULL, br = 0ULL;
+        uint32_t bi = 0xffffffffu, bm = (RZ << 20) | (RZ << 26);
+        int bs = 0;
+        for (int s = 0; s < hbw; ++s) {
+            const int o = s * T + tid;
+            const unsigned long long es = rE[o];
+            const unsigned long long rs = rR[o];
+            const unsigned long long mt = rM[o];
+            // slots past this lane's count may hold stale or never-written words
+            const uint32_t m = s < nr ? static_cast<uint32_t>(mt) : ((RZ << 20) | (RZ << 26));
+            const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
+            const unsigned long long c1 = dbits(clk[i1 * T + tid]);
+            const unsigned long long c2 = dbits(clk[i2 * T + tid]);
+            unsigned long long e = es > c1 ? es : c1;
+            e = e > c2 ? e : c2;
+            const uint32_t id = (COLO && e == es) ? static_cast<uint32_t>(mt >> 32) : (m & MP_NODE_MASK);
+            const bool take = !done && s < nr && key_less_nb(e, rs, id, be, br, bi);
+            be = take ? e : be;
+            br = take ? rs : br;
+            bi = take ? id : bi;
+            bm = take ? m : bm;
+            bs = take ? s : bs;
+        }
+        const double bd = done ? 0.0 : rD[bs * T + tid];
+        // unordered removal: the last entry moves into the hole
+        const int last = nr - 1;
+        if (!done && bs != last) {
+            const int o = bs * T + tid, ol = last * T + tid;
+            rE[o] = rE[ol];
+            rR[o] = rR[ol];
+            rM[o] = rM[ol];
+            rD[o] = rD[ol];
+        }
+        nr = done ? nr : last;
+        // -- commit (solver.py:130-138) ------------------------------------------------
+        const double end = bitsd(be) + bd;
+        const int node = static_cast<int>(bm & MP_NODE_MASK);
+        const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+        if (!done) {
+            clk[(r1 == RZ ? WS : r1) * T + tid] = end;
+            clk[(r2 == RZ ? WS : r2) * T + tid] = end;
+        }
+        const bool isop = node < n_ops;
+        ms = (!done && isop && end > ms) ? end : ms;
+        // -- successors (solver.py:140-145), one uniform loop over the warp's
+        //    largest successor count: op -> its out-flows, flow -> its consumer ---------
+        const int d = static_cast<int>(r1);
+        const int nodec = done ? 0 : node;
+        const int ob = static_cast<int>(T_out_beg[isop ? nodec : 0]);
+        const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
+        const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
+        const int maxc = __reduce_max_sync(kFull, cnt);
+        for (int t = 0; t < maxc; ++t) {
+            const bool act = t < cnt;
+            const int q = (act && isop) ? ob + t : 0;
+            const double2 rec = T_rec[q];
+            const unsigned long long rb = dbits(rec.x);
+            const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+            const int dj = rowt[j * T + tid];
+            const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
+            const bool cross = dj != d;
+            const bool via_colo = COLO && isop && !cross;
+            const bool flow_ins = act && isop && !via_colo;  // a flow enters the ready set
+            const bool op_upd = act && !flow_ins;            // j's npred / est / gate change
+            const bool fcross = isop && cross;
+            const int bi2 = fcross ? d * K + dj : 0;
+            const double fdur = fcross ? div_bw(rec.y, T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+            const double rj = g_rank[static_cast<long long>(j) * L];
+            const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                   (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                : ((RZ << 20) | (RZ << 26)));
+            // multi-input ops keep npred / est / gate id
+            const uint32_t k = T_mi[j];
+            const bool multi = k != MP_NONE;
+            const bool mupd = op_upd && multi;
+            const long long mo = static_cast<long long>(multi ? k : 0) * L;
+            uint32_t np1 = 1u, ct = 0u;
+            double cur = 0.0;
+            if (mupd) {
+                np1 = g_mnp[mo];
+                cur = g_mest[mo];
+                ct = g_mtie[mo];
+            }
+            const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+            const uint32_t np = np1 - 1u;
+            const bool up = end > cur;
+            const double ej = multi ? (up ? end : cur) : end;
+            const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
+            const uint32_t tie_j = multi ? tie_new : tj;
+            if (mupd) {
+                g_mnp[mo] = np;
+                g_mest[mo] = ej;
+                g_mtie[mo] = tie_new;
+            }
+            const bool op_ins = op_upd && (!multi || np == 0u);
+            const double odur = T_cost[j * K + dj];
+            insert(flow_ins || op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
+                   flow_ins ? fdur : odur,
+                   flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                   flow_ins ? pid : tie_j);
+        }
+        done = done || ovf || nr == 0;
+    }
+    r.ms = ms;
+    r.status = status;
+    r.over_dev = over_dev;
+    r.over_by = over_by;
+    r.ovf = ovf;
+    return r;
+}
+
 template <int RC, bool COLO>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1119,6 +1346,99 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_ls_kernel(const 
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
             if (live) v.rowt[i * T + tid] = static_cast<unsigned char>(nd);
             const TppResult r = tpp_eval<RC, COLO>(v, a, live, false, a.rcap);
+            const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
+            if (!r.ovf && ms <= cur_ms) {
+                cur_ms = ms;
+            } else if (live) {
+                v.rowt[i * T + tid] = static_cast<unsigned char>(old);
+            }
+        }
+        if (live) {
+            for (int i = 0; i < n; ++i) ls.chain_rows[c * n + i] = v.rowt[i * T + tid];
+            ls.chain_ms[c] = cur_ms;
+        }
+        __syncwarp();
+    }
+}
+
+// ---- thread per placement, ready set in shared memory ----------------------------------
+template <bool COLO>
+__global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __grid_constant__ EvalArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ double s_best_ms[MP_TPP_MAX_THREADS / 32];
+    __shared__ long long s_best_row[MP_TPP_MAX_THREADS / 32];
+    const int lane = threadIdx.x & 31;
+    stage_tables(sm, a, &s_bar);
+    const TppView v = tpp_view(a, sm);
+    const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
+    double best_ms = kInf;
+    long long best_row = LLONG_MAX;
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next, 32ULL);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= static_cast<unsigned long long>(n_rows)) break;
+        const unsigned long long p = base + lane;
+        const bool live = p < static_cast<unsigned long long>(n_rows);
+        const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
+        const long long grow = a.row_base + lrow;
+        const bool bad = tpp_load_row(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
+        const TppResult r = tpps_eval<COLO>(v, a, live, bad, a.rcap);
+        if (live) {
+            const long long o = grow - a.out_base;
+            if (r.ovf) {
+                const unsigned int k = atomicAdd(a.ovf_count, 1u);
+                a.ovf_rows[k] = grow;
+                if (a.status) a.status[o] = MP_ROW_OVERFLOW;
+            } else {
+                const double ms = r.alive ? r.ms : kInf;
+                if (a.makespan) a.makespan[o] = ms;
+                if (a.status) a.status[o] = static_cast<int8_t>(r.status);
+                if (a.mem_dev) a.mem_dev[o] = r.over_dev;
+                if (a.overflow) a.overflow[o] = r.over_by;
+                if (r.alive && (ms < best_ms || (ms == best_ms && grow < best_row))) {
+                    best_ms = ms;
+                    best_row = grow;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (a.want_argmin) cta_keep_best(a, best_ms, best_row, s_best_ms, s_best_row);
+}
+
+// K5 on the thread-per-placement layout (shared-memory ready set): one lane per chain, the chain's row in
+// its tile column.  Same proposals, acceptance rule and ready capacity (`a.rcap`,
+// the group kernel's) as mp_ls_kernel, so results do not depend on the kernel.
+template <bool COLO>
+__global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const __grid_constant__ EvalArgs a,
+                                                                         const __grid_constant__ LsArgs ls) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    const int lane = threadIdx.x & 31;
+    stage_tables(sm, a, &s_bar);
+    const TppView v = tpp_view(a, sm);
+    const int n = a.n_ops, K = a.K, T = v.T, tid = v.tid;
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next, 32ULL);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= static_cast<unsigned long long>(ls.n_chains)) break;
+        const unsigned long long c = base + lane;
+        const bool live = c < static_cast<unsigned long long>(ls.n_chains);
+        const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
+        const long long srow = live ? static_cast<long long>(gc % static_cast<unsigned long long>(ls.n_seed)) : 0;
+        tpp_load_row(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
+        const TppResult r0 = tpps_eval<COLO>(v, a, live, false, a.rcap);
+        double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
+        for (int t = 0; t < ls.moves && K > 1; ++t) {
+            const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
+            const int i = static_cast<int>((h & 0xffffffffULL) % static_cast<unsigned long long>(n));
+            const int old = v.rowt[i * T + tid];
+            const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
+            if (live) v.rowt[i * T + tid] = static_cast<unsigned char>(nd);
+            const TppResult r = tpps_eval<COLO>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
                 cur_ms = ms;
@@ -1325,6 +1645,38 @@ cudaError_t mp_launch_tpp_ls(int rc, int threads, int ctas, int smem, const Eval
     LsFn f = rc <= 4 ? (a.colo ? mp_tpp_ls_kernel<4, true> : mp_tpp_ls_kernel<4, false>)
                      : (rc <= 8 ? (a.colo ? mp_tpp_ls_kernel<8, true> : mp_tpp_ls_kernel<8, false>)
                                 : (a.colo ? mp_tpp_ls_kernel<16, true> : mp_tpp_ls_kernel<16, false>));
+    f<<<ctas, threads, smem, s>>>(a, ls);
+    ++g_mp_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        for (EvalFn f : {mp_tpps_kernel<true>, mp_tpps_kernel<false>}) {
+            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    EvalFn f = a.colo ? mp_tpps_kernel<true> : mp_tpps_kernel<false>;
+    f<<<ctas, threads, smem, s>>>(a);
+    ++g_mp_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        for (LsFn f : {mp_tpps_ls_kernel<true>, mp_tpps_ls_kernel<false>}) {
+            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    LsFn f = a.colo ? mp_tpps_ls_kernel<true> : mp_tpps_ls_kernel<false>;
     f<<<ctas, threads, smem, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();

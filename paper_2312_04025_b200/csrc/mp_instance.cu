@@ -339,6 +339,8 @@ struct mp_instance {
     DevBuf main_state, wide_state;
     // thread-per-placement variant (mp_tpp_kernel); tpp_rc == 0: not used
     bool tpp_allowed = true;
+    bool tpp_smem_pref = false;  // MP_TUNE_TPP_SMEM: shared-memory ready set even when registers fit
+    int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
     DevBuf tpp_state;
     // per-call scratch
@@ -447,26 +449,51 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         I->main_so = so;
         I->main_rcap = rcap;
     }
-    // thread-per-placement variant: automatic shape, small calibrated ready set,
-    // instance tables + per-lane row and clocks in shared memory
+    // thread-per-placement variants: automatic shape, calibrated ready set, instance
+    // tables + per-lane row and clocks (+ ready entries) in shared memory
     I->tpp_rc = 0;
+    I->tpp_kind = 0;
     if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
-        // register capacity: the smallest template >= the calibrated peak (not 2x: a
-        // register slot costs a select per field on every insertion; rows that
-        // outgrow it are re-run exactly by the off-chip variant)
         const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
-        const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
-        const long long per_lane = n_ops + 8LL * (3 * K + 2);
         const long long avail = static_cast<long long>(smem_cap) - I->to.bytes - 32;
-        const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
-        if (rc > 0 && T >= 128) {
+        const long long base_lane = n_ops + 8LL * (3 * K + 2);
+        // shared-memory ready set: 32 B per entry per lane, capacity = the peak (>= 4)
+        const int cap_s = ready_cap_req > 0 ? rcap : std::min(I->ready_bound, std::max(4, want));
+        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS,
+                                                            std::max(0LL, avail / (base_lane + 32LL * cap_s)) / 32 * 32));
+        // register ready set: the smallest template >= the peak
+        const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
+        const int Tr = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / base_lane) / 32 * 32));
+        // registers first (measured faster when the peak fits a template: C2 40.9 vs
+        // 31.4 M/s), the shared-memory ready set for wider peaks (C1: 12.4 vs 8.2 M/s
+        // for the group kernel)
+        const bool prefer_smem = I->tpp_smem_pref;
+        if (rc > 0 && Tr >= 128 && !prefer_smem) {
+            I->tpp_kind = 1;
             I->tpp_rc = rc;
-            I->tpp_threads = T;
-            I->tpp_ctas = std::min(I->sms, I->main.ctas);
-            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * T + 15) & ~15LL) +
-                                           8LL * (3 * K + 2) * T);
+            I->tpp_threads = Tr;
+            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * Tr + 15) & ~15LL) +
+                                           8LL * (3 * K + 2) * Tr);
+        } else if (Ts >= 128) {
+            I->tpp_kind = 2;
+            I->tpp_rc = cap_s;
+            I->tpp_threads = Ts;
+            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * Ts + 15) & ~15LL) +
+                                           (8LL * (3 * K + 2) + 32LL * cap_s) * Ts);
         }
+        I->tpp_ctas = std::min(I->sms, I->main.ctas);
     }
+}
+
+// thread-per-placement shape with a shared-memory ready set of capacity `cap`
+// (local search runs at the group kernel's capacity); threads = 0 if it does not fit
+void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
+    const long long avail = static_cast<long long>(MP_SMEM_DYN_MAX) - I->to.bytes - 32;
+    const long long per_lane = I->n_ops + 8LL * (3 * I->K + 2) + 32LL * cap;
+    const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
+    *threads = T >= 64 ? T : 0;
+    *smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(I->n_ops) * T + 15) & ~15LL) + per_lane * T -
+                             static_cast<long long>(I->n_ops) * T);
 }
 
 // ready capacity of the variant that runs first (rows beyond it re-run off-chip)
@@ -837,6 +864,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->table_bytes = I->to.bytes;
     info->state_bytes = I->main_so.bytes;
     info->tpp_ready_cap = I->tpp_rc;
+    info->tpp_kind = I->tpp_kind;
     info->tpp_threads = I->tpp_rc > 0 ? I->tpp_threads : 0;
     return MP_OK;
 }
@@ -855,6 +883,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->rcap_target = ready_cap > 0 ? ready_cap : (I->peak_probe > 0 ? std::max(4, 2 * I->peak_probe) : 32);
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
+    I->tpp_smem_pref = (flags & MP_TUNE_TPP_SMEM) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }
@@ -954,7 +983,12 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
     if (I->tpp_rc > 0) {
         a.lane_stride = static_cast<long long>(I->tpp_ctas) * I->tpp_threads;
         a.gstate = static_cast<unsigned char *>(I->tpp_state.p);
-        if ((e = mp_launch_tpp(I->tpp_rc, I->tpp_threads, I->tpp_ctas, I->tpp_smem, a, s)) != cudaSuccess) return e;
+        if (I->tpp_kind == 2) {
+            a.rcap = I->tpp_rc;
+            if ((e = mp_launch_tpps(I->tpp_threads, I->tpp_ctas, I->tpp_smem, a, s)) != cudaSuccess) return e;
+        } else if ((e = mp_launch_tpp(I->tpp_rc, I->tpp_threads, I->tpp_ctas, I->tpp_smem, a, s)) != cudaSuccess) {
+            return e;
+        }
     } else if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) {
         return e;
     }
@@ -1276,7 +1310,14 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     // thread-per-placement chains when the instance has a TPP shape and the group
     // kernel's capacity fits a register template (same capacity -> same results)
     const int ls_rc = I->main_rcap <= 4 ? 4 : (I->main_rcap <= 8 ? 8 : (I->main_rcap <= 16 ? 16 : 0));
-    if (I->tpp_rc > 0 && ls_rc > 0) {
+    int ls_T = 0, ls_smem = 0;
+    if (I->tpp_kind == 2) tpps_shape(I, I->main_rcap, &ls_T, &ls_smem);
+    if (I->tpp_kind == 2 && ls_T > 0) {
+        MP_CUDA(I->tpp_state.ensure(mp_tpp_state_bytes(I->n_ops, I->n_multi, static_cast<long long>(I->tpp_ctas) * ls_T)));
+        a.lane_stride = static_cast<long long>(I->tpp_ctas) * ls_T;
+        a.gstate = static_cast<unsigned char *>(I->tpp_state.p);
+        MP_CUDA(mp_launch_tpps_ls(ls_T, I->tpp_ctas, ls_smem, a, ls, s));
+    } else if (I->tpp_rc > 0 && ls_rc > 0) {
         MP_CUDA(I->tpp_state.ensure(mp_tpp_state_bytes(I->n_ops, I->n_multi, static_cast<long long>(I->tpp_ctas) * I->tpp_threads)));
         a.lane_stride = static_cast<long long>(I->tpp_ctas) * I->tpp_threads;
         a.gstate = static_cast<unsigned char *>(I->tpp_state.p);
