@@ -16,6 +16,9 @@ import numpy as np
 from . import errors as E
 
 LIB_PATH = Path(__file__).resolve().parent / "libmoirai_b200.so"
+# developer override for A/B builds of the same library (never needed in normal use)
+if os.environ.get("MOIRAI_B200_LIB"):
+    LIB_PATH = Path(os.environ["MOIRAI_B200_LIB"])
 
 MP_OK = 0
 MP_ERR_INVALID = -1
