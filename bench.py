@@ -330,7 +330,10 @@ def run_ours(args):
                 "traffic": (tr["dram_bytes_per_row"] * P if tr and "dram_bytes_per_row" in tr else None),
                 "traffic_source": (tr or {}).get("source"), "peak_source": peak_kind,
                 "algorithmic_bytes_per_placement": bytes_per, "kernel_ms": t_kern * 1e3,
-                "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan"}
+                "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan",
+                "issue_bound_evidence": ({k: tr[k] for k in ("ipc_active", "issue_slots_busy", "active_threads_per_warp",
+                                                             "l2_hit_rate", "achieved_warps_per_sm") if k in tr}
+                                         if tr else None)}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,

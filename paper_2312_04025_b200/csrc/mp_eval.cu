@@ -1243,54 +1243,84 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
         const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
         const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
         const int maxc = __reduce_max_sync(kFull, cnt);
-        for (int t = 0; t < maxc; ++t) {
-            const bool act = t < cnt;
-            const int q = (act && isop) ? ob + t : 0;
-            const double2 rec = T_rec[q];
-            const unsigned long long rb = dbits(rec.x);
-            const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
-            const int dj = rowt[j * T + tid];
-            const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
-            const bool cross = dj != d;
-            const bool via_colo = COLO && isop && !cross;
-            const bool flow_ins = act && isop && !via_colo;  // a flow enters the ready set
-            const bool op_upd = act && !flow_ins;            // j's npred / est / gate change
-            const bool fcross = isop && cross;
-            const int bi2 = fcross ? d * K + dj : 0;
-            const double fdur = fcross ? div_bw(rec.y, T_bw[bi2], T_rbw[bi2], fast) : 0.0;
-            const double rj = g_rank[static_cast<long long>(j) * L];
-            const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
-                                                   (static_cast<uint32_t>(2 * K + dj) << 26))
-                                                : ((RZ << 20) | (RZ << 26)));
-            // multi-input ops keep npred / est / gate id
-            const uint32_t k = T_mi[j];
-            const bool multi = k != MP_NONE;
-            const bool mupd = op_upd && multi;
-            const long long mo = static_cast<long long>(multi ? k : 0) * L;
-            uint32_t np1 = 1u, ct = 0u;
-            double cur = 0.0;
-            if (mupd) {
-                np1 = g_mnp[mo];
-                cur = g_mest[mo];
-                ct = g_mtie[mo];
+        // Successors are processed SU at a time: every global load of the group
+        // (rank of the consumer, multi-input state) is issued before any of them is
+        // used, so their latencies overlap.  The consumers of one step are distinct
+        // (no parallel edges), so the hoisted loads never read a value written
+        // earlier in the same group.
+        constexpr int SU = 2;
+        for (int t0 = 0; t0 < maxc; t0 += SU) {
+            int j_[SU], dj_[SU];
+            uint32_t pid_[SU], np1_[SU], ct_[SU];
+            long long mo_[SU];
+            double rj_[SU], cur_[SU], pay_[SU];
+            bool act_[SU], multi_[SU];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                const int t = t0 + u;
+                const bool act = t < cnt;
+                const int q = (act && isop) ? ob + t : 0;
+                const double2 rec = T_rec[q];
+                const unsigned long long rb = dbits(rec.x);
+                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                j_[u] = j;
+                dj_[u] = rowt[j * T + tid];
+                pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
+                pay_[u] = rec.y;
+                act_[u] = act;
+                rj_[u] = g_rank[static_cast<long long>(j) * L];
+                const uint32_t k = T_mi[j];
+                multi_[u] = k != MP_NONE;
+                mo_[u] = static_cast<long long>(multi_[u] ? k : 0) * L;
+                const bool op_upd = act && !(isop && !(COLO && dj_[u] == d));
+                np1_[u] = 1u;
+                cur_[u] = 0.0;
+                ct_[u] = 0u;
+                if (op_upd && multi_[u]) {
+                    np1_[u] = g_mnp[mo_[u]];
+                    cur_[u] = g_mest[mo_[u]];
+                    ct_[u] = g_mtie[mo_[u]];
+                }
             }
-            const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
-            const uint32_t np = np1 - 1u;
-            const bool up = end > cur;
-            const double ej = multi ? (up ? end : cur) : end;
-            const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
-            const uint32_t tie_j = multi ? tie_new : tj;
-            if (mupd) {
-                g_mnp[mo] = np;
-                g_mest[mo] = ej;
-                g_mtie[mo] = tie_new;
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                if (t0 + u >= maxc) break;
+                const int j = j_[u], dj = dj_[u];
+                const uint32_t pid = pid_[u];
+                const bool act = act_[u], multi = multi_[u];
+                const bool cross = dj != d;
+                const bool via_colo = COLO && isop && !cross;
+                const bool flow_ins = act && isop && !via_colo;  // a flow enters the ready set
+                const bool op_upd = act && !flow_ins;            // j's npred / est / gate change
+                const bool fcross = isop && cross;
+                const int bi2 = fcross ? d * K + dj : 0;
+                const double fdur = fcross ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                const double rj = rj_[u];
+                const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                       (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                    : ((RZ << 20) | (RZ << 26)));
+                // multi-input ops keep npred / est / gate id
+                const bool mupd = op_upd && multi;
+                const double cur = cur_[u];
+                const uint32_t ct = ct_[u];
+                const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+                const uint32_t np = np1_[u] - 1u;
+                const bool up = end > cur;
+                const double ej = multi ? (up ? end : cur) : end;
+                const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
+                const uint32_t tie_j = multi ? tie_new : tj;
+                if (mupd) {
+                    g_mnp[mo_[u]] = np;
+                    g_mest[mo_[u]] = ej;
+                    g_mtie[mo_[u]] = tie_new;
+                }
+                const bool op_ins = op_upd && (!multi || np == 0u);
+                const double odur = T_cost[j * K + dj];
+                insert(flow_ins || op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
+                       flow_ins ? fdur : odur,
+                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                       flow_ins ? pid : tie_j);
             }
-            const bool op_ins = op_upd && (!multi || np == 0u);
-            const double odur = T_cost[j * K + dj];
-            insert(flow_ins || op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
-                   flow_ins ? fdur : odur,
-                   flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
-                   flow_ins ? pid : tie_j);
         }
         done = done || ovf || nr == 0;
     }
