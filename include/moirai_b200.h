@@ -50,6 +50,7 @@ extern "C" {
 #define MP_ERR_MEMORY_EXCEEDED  -8  /* MemoryExceededError(device, overflow) solver.py:85-87  */
 #define MP_ERR_BAD_DEVICE       -9  /* KeyError: placement names an unknown device solver.py:163 */
 #define MP_ERR_NO_GPU          -10  /* no CUDA device visible                                 */
+#define MP_ERR_INFEASIBLE_MEMORY -11 /* InfeasibleMemoryError(needed=a, available=b) baselines.py:75-77 */
 
 /* per-row status written by the batched calls */
 #define MP_ROW_OK          0
@@ -197,6 +198,34 @@ int32_t mp_branch_and_bound(mp_instance *inst, const int32_t *op_order, double g
                             const uint8_t *seed_rows, int32_t n_seed,
                             uint8_t *best_row, double *best_ms, int32_t *solve_status,
                             int64_t *visited, mp_error *err);
+
+/* ---- greedy baselines (replaces greedy_place, baselines.py:27-86) ---------
+ * One warp, lane k scores device k; ops in `op_order` (topo_order(gc)).  kind 0
+ * = EARLIEST_FINISH, 1 = EARLIEST_START.  `row` receives the device index of each
+ * op; the caller schedules it (mp_schedule_one) exactly as the reference's final
+ * `_schedule` call.  MP_ERR_INFEASIBLE_MEMORY when no device can hold an op. */
+int32_t mp_greedy_place(mp_instance *inst, const int32_t *op_order, int32_t kind,
+                        uint8_t *row, mp_error *err);
+
+/* ---- schedule audit (replaces check_feasibility, simulator.py:179-264) ----
+ * starts/ends: [n_ops + n_flows] node times (index = node index).  Violations are
+ * returned in the reference's report order; *n_out = their number (only the first
+ * out_cap are written).  kind / x / y:
+ *   0 memory-over          x = device index, y = load
+ *   1 duration-mismatch    x = node index
+ *   2 negative start       x = node index      (reported as duration-mismatch)
+ *   3 precedence-break     x = link index (2f: src->flow f, 2f+1: flow f->dst)
+ *   4 device-overlap       x, y = op indices (x < y)
+ *   5 source-channel       x, y = flow indices (x < y)
+ *   6 dest-channel         x, y = flow indices (x < y)                        */
+typedef struct mp_violation {
+    int32_t kind;
+    int32_t pad;
+    int64_t x, y;
+} mp_violation;
+int32_t mp_audit_schedule(mp_instance *inst, const uint8_t *row, const double *starts,
+                          const double *ends, double tol, mp_violation *out, int64_t out_cap,
+                          int64_t *n_out, mp_error *err);
 
 /* ---- GCOF coarsening (K1/K2; replaces gcof, fusion.py:271-304) ----------- */
 typedef struct mp_coarsen_input {

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 LIB = PKG / "libmoirai_b200.so"
 OBJ = PKG / "_obj"
 
-SOURCES = ["mp_eval.cu", "mp_instance.cu", "mp_bnb.cu", "mp_coarsen.cu"]
+SOURCES = ["mp_eval.cu", "mp_instance.cu", "mp_bnb.cu", "mp_aux.cu", "mp_coarsen.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",
            "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]

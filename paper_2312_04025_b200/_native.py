@@ -31,6 +31,7 @@ MP_ERR_CUDA = -7
 MP_ERR_MEMORY_EXCEEDED = -8
 MP_ERR_BAD_DEVICE = -9
 MP_ERR_NO_GPU = -10
+MP_ERR_INFEASIBLE_MEMORY = -11
 
 MP_ROW_OK = 0
 MP_ROW_MEMORY = 1
@@ -69,6 +70,10 @@ class mp_instance_info(C.Structure):
         ("table_bytes", C.c_int64), ("state_bytes", C.c_int64),
         ("tpp_ready_cap", C.c_int32), ("tpp_threads", C.c_int32), ("tpp_kind", C.c_int32),
     ]
+
+
+class mp_violation(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("x", C.c_int64), ("y", C.c_int64)]
 
 
 class mp_coarsen_input(C.Structure):
@@ -123,6 +128,9 @@ SIGNATURES = {
     "mp_branch_and_bound": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_double,
                                          C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double),
                                          C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(mp_error)]),
+    "mp_greedy_place": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(mp_error)]),
+    "mp_audit_schedule": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                       C.c_int64, C.POINTER(C.c_int64), C.POINTER(mp_error)]),
     "mp_coarsen": (C.c_int32, [C.POINTER(mp_coarsen_input), C.c_int32, C.POINTER(mp_coarsen_output),
                                C.POINTER(mp_error)]),
     "mp_coarsen_free": (None, [C.POINTER(mp_coarsen_output)]),
@@ -170,6 +178,8 @@ def check(code: int, err: mp_error, context: str = "") -> None:
         raise E.TooLargeError(int(err.a), int(err.b))
     if code == MP_ERR_INVALID:
         raise ValueError(f"{context}: {msg}")
+    if code == MP_ERR_INFEASIBLE_MEMORY:
+        raise E.InfeasibleMemoryError(int(err.a), int(err.b))
     if code == MP_ERR_BAD_DEVICE:
         raise KeyError(f"{context}: {msg}")
     raise E.NativeError(f"{context}: status {code}: {msg}")

@@ -21,8 +21,8 @@ from typing import Iterable, Iterator
 import numpy as np
 
 from . import _native as N
-from .errors import CycleError, UnknownEdgeError
-from .graph import CompGraph, FlowEdge, OpNode, Tag, _make_edge, _make_opnode, find_cycle
+from .errors import CycleCreationError, CycleError, UnknownEdgeError
+from .graph import CompGraph, FlowEdge, OpNode, Tag, _make_edge, _make_opnode, find_cycle, validate_dag
 from .profiles import CostOverrides
 
 FUSE_JOINER = "∘"  # joins member types in a fused node's op_type (fusion.py:23)
@@ -243,3 +243,56 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         gid_of.append(gid)
     edges = [_make_edge(gid_of[u], gid_of[v], p) for u, v, p in zip(esrc.tolist(), edst.tolist(), epay.tolist())]
     return CompGraph._trusted(new_nodes, edges)
+
+
+def _combined_cost(parts, seq, overrides):
+    """Per-device time of a fused node (``fusion.py:117-130``): override, else
+    the builtin ``sum`` of the member times in member order."""
+    common = set(parts[0].compute_time)
+    for p in parts[1:]:
+        common &= set(p.compute_time)
+    devices = set(common)
+    if overrides is not None:
+        devices |= overrides.devices_for(seq)
+    cost = {}
+    for k in sorted(devices):
+        ov = overrides.get(seq, k) if overrides is not None else None
+        cost[k] = ov if ov is not None else sum(p.compute_time[k] for p in parts)
+    return cost
+
+
+def fuse(g: CompGraph, pred: int, succ: int, overrides: CostOverrides | None = None) -> tuple[CompGraph, OpNode]:
+    """Fuse one edge (``fusion.py:251-268``): the merged node (id = min of the
+    two, members / type sequence concatenated pred first, memory summed, costs
+    summed or overridden, tag FUSED) takes the union of both endpoints' external
+    edges; the edge list comes back sorted by ``(u, v)`` as the reference's
+    ``materialize``.  ``UnknownEdgeError`` when the edge is missing,
+    ``CycleCreationError`` when another pred ~> succ path would close a cycle.
+    A single graph edit, not a data-parallel path: it runs on the host."""
+    if g.edge(pred, succ) is None:
+        raise UnknownEdgeError(pred, succ)
+    validate_dag(g)
+    frontier = [n for n in g.succs(pred) if n != succ]
+    seen = set(frontier)
+    while frontier:
+        n = frontier.pop()
+        if n == succ:
+            raise CycleCreationError(pred, succ)
+        for m in g.succs(n):
+            if m not in seen:
+                seen.add(m)
+                frontier.append(m)
+    a, b = g.node(pred), g.node(succ)
+    seq = a.type_seq + b.type_seq
+    gid = min(pred, succ)
+    merged = OpNode(gid, FUSE_JOINER.join(seq), a.mem_bytes + b.mem_bytes, _combined_cost([a, b], seq, overrides),
+                    a.members + b.members, seq, Tag.FUSED)
+    nodes = [merged if n.id == gid else n for n in g.nodes if n.id not in (pred, succ) or n.id == gid]
+    where = {pred: gid, succ: gid}
+    payload: dict[tuple[int, int], int] = {}
+    for e in g.edges:
+        gu, gv = where.get(e.src, e.src), where.get(e.dst, e.dst)
+        if gu != gv:
+            payload[(gu, gv)] = payload.get((gu, gv), 0) + e.payload_bytes
+    out = CompGraph(sorted(nodes, key=lambda n: n.id), [FlowEdge(u, v, payload[(u, v)]) for (u, v) in sorted(payload)])
+    return out, out.node(gid)

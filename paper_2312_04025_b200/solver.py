@@ -314,7 +314,8 @@ def solve_exact(gc: CompGraph, c: Cluster, mesh: EffectiveMesh,
       incumbent, or ``Status.BUDGET`` without one (``solver.py:246-254``).
 
     The incumbent is seeded with a GPU local search (``seed_chains`` chains from
-    seeded random rows); at gap 0 seeds change the work, never the answer.
+    seeded random rows and the two greedy baselines); at gap 0 seeds change the
+    work, never the answer.
     """
     budget = budget or SolveBudget()
     with Instance(gc, c, mesh) as inst:
@@ -327,7 +328,16 @@ def solve_exact(gc: CompGraph, c: Cluster, mesh: EffectiveMesh,
             rng = np.random.Generator(np.random.PCG64(0x5eed))
             start = rng.integers(0, k, (min(seed_chains, 64), n), dtype=np.uint8)
             moves = seed_moves if seed_moves is not None else min(4 * n * k, 2048)
-            row, ms, _, _ = local_search(inst, start, chains=seed_chains, moves=moves, seed=1)
+            from .baselines import BaselineKind, greedy_row
+            from .errors import InfeasibleMemoryError
+
+            cand = [start]
+            for kind in BaselineKind:  # the reference's greedy baselines as extra starting points
+                try:
+                    cand.append(greedy_row(inst, kind).reshape(1, n))
+                except InfeasibleMemoryError:
+                    pass
+            row, ms, _, _ = local_search(inst, np.concatenate(cand), chains=seed_chains, moves=moves, seed=1)
             if math.isfinite(ms):
                 seeds = row.reshape(1, n)
         best = np.zeros(n, dtype=np.uint8)

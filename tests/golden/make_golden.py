@@ -294,6 +294,116 @@ def make_solve_exact():
     return cases
 
 
+def _ser_sched(s):
+    return {"assignment": {str(k): v for k, v in s.assignment.items()},
+            "starts": {str(k): H(v) for k, v in s.starts.items()}, "ends": {str(k): H(v) for k, v in s.ends.items()},
+            "channels": {str(k): (list(v) if v else None) for k, v in s.channels.items()}, "makespan": H(s.makespan_s)}
+
+
+def make_aux():
+    """greedy_place (baselines.py:27-86), check_feasibility (simulator.py:179-264)
+    and fuse (fusion.py:251-268) outputs of the reference."""
+    import copy
+
+    from opplace import baselines as rb
+    from opplace import simulator as rs
+
+    greedy, audit, fuse = [], [], []
+
+    def add_greedy(tag, g, c):
+        mesh = ref.effective_bandwidth(c)
+        for kind in (rb.BaselineKind.EARLIEST_FINISH, rb.BaselineKind.EARLIEST_START):
+            rec = {"name": tag, "kind": kind.value, "graph": ser_graph(g), "cluster": ser_cluster(c)}
+            try:
+                rec["schedule"] = _ser_sched(rb.greedy_place(g, c, mesh, kind))
+            except ref.InfeasibleMemoryError as e:
+                rec["error"] = [e.needed, e.available]
+            greedy.append(rec)
+
+    for trial in range(50):
+        g, c = rc.random_instance(random.Random(9001 + trial), max_ops=8, tight_ok=True, min_ops=3)
+        add_greedy(f"acc-{9001 + trial}", g, c)
+    for trial in range(20):
+        g, c = rc.random_instance(random.Random(700 + trial), max_ops=12, tight_ok=True, min_ops=6)
+        add_greedy(f"rnd-{700 + trial}", g, c)
+    for name in ("two_op_chain", "split_chain", "skewed_pair"):
+        g, c = getattr(rc, name)()
+        add_greedy(name, g, c)
+    for w in (workloads.c1(), workloads.c2(4)):
+        add_greedy(w.name, ref.gcof(to_ref_graph(w.raw), to_ref_rules(w.rules)), to_ref_cluster(w.cluster))
+
+    def add_audit(tag, g, c, sched, tol=0.0):
+        mesh = ref.effective_bandwidth(c)
+        out = rs.check_feasibility(sched, g, c, mesh, tol)
+        audit.append({"name": tag, "graph": ser_graph(g), "cluster": ser_cluster(c), "schedule": _ser_sched(sched),
+                      "tol": H(tol), "violations": [[v.kind.value, v.details, list(v.nodes)] for v in out]})
+
+    for trial in range(30):
+        rng = random.Random(3000 + trial)
+        g, c = rc.random_instance(rng, tight_ok=trial % 3 == 0)
+        mesh = ref.effective_bandwidth(c)
+        assign = {i: rng.choice(c.device_ids) for i in g.node_ids}
+        try:
+            sched = ref.schedule_for_assignment(g, c, mesh, assign)
+        except ref.MemoryExceededError:
+            continue
+        add_audit(f"clean-{trial}", g, c, sched)
+        # deterministic corruptions of the canonical schedule
+        nodes = sorted(sched.starts)
+        for m in range(4):
+            bad = copy.deepcopy(sched)
+            pick = nodes[(trial * 7 + m * 3) % len(nodes)]
+            if m == 0:      # shift a node earlier: precedence / overlap breaks
+                bad.starts[pick] -= 0.75
+                bad.ends[pick] -= 0.75
+            elif m == 1:    # stretch a node: duration mismatch
+                bad.ends[pick] += 0.5
+            elif m == 2:    # pull everything to time zero: overlaps everywhere
+                for n in nodes:
+                    d = bad.ends[n] - bad.starts[n]
+                    bad.starts[n] = 0.0
+                    bad.ends[n] = d
+            else:           # negative start
+                bad.starts[pick] = -1.0
+            add_audit(f"bad-{trial}-{m}", g, c, bad)
+            if m == 1:
+                add_audit(f"bad-{trial}-{m}-tol", g, c, bad, tol=0.6)
+    # memory over: the same schedule audited against a smaller cluster
+    g, c = rc.random_instance(random.Random(3100), tight_ok=False)
+    mesh = ref.effective_bandwidth(c)
+    sched = ref.schedule_for_assignment(g, c, mesh, {i: c.device_ids[0] for i in g.node_ids})
+    small = ref.Cluster([ref.Device(d.id, 1) for d in c.devices], dict(c.links))
+    add_audit("memory-over", g, small, sched)
+
+    def add_fuse(tag, g, a, b, ov=None):
+        rec = {"name": tag, "graph": ser_graph(g), "pred": a, "succ": b,
+               "overrides": None if ov is None else [[list(s), k, H(t)] for (s, k), t in ov.entries.items()]}
+        try:
+            out, merged = ref.fuse(g, a, b, ov)
+            rec["out"] = ser_graph(out)
+            rec["merged"] = merged.id
+        except ref.OpPlaceError as e:
+            rec["error"] = type(e).__name__
+        fuse.append(rec)
+
+    rb_g = rc.residual_block()
+    for e in rb_g.edges:
+        add_fuse(f"residual-{e.src}-{e.dst}", rb_g, e.src, e.dst)
+    add_fuse("residual-missing", rb_g, 9, 1)
+    for seed in range(20):
+        g = rc.random_dag(random.Random(seed), max_ops=10)
+        for e in g.edges[:4]:
+            add_fuse(f"dag-{seed}-{e.src}-{e.dst}", g, e.src, e.dst)
+    tri = ref.CompGraph([ref.OpNode(1, "conv", 1, {0: 1.0}), ref.OpNode(2, "bn", 1, {0: 1.0}),
+                         ref.OpNode(3, "relu", 1, {0: 1.0})],
+                        [ref.FlowEdge(1, 2, 1), ref.FlowEdge(2, 3, 1), ref.FlowEdge(1, 3, 1)])
+    add_fuse("triangle", tri, 1, 3)
+    two = ref.CompGraph([ref.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}), ref.OpNode(2, "bn", 5, {0: 3.0, 1: 1.0})],
+                        [ref.FlowEdge(1, 2, 100)])
+    add_fuse("override", two, 1, 2, ref.CostOverrides({(("conv", "bn"), 0): 3.5}))
+    return {"greedy": greedy, "audit": audit, "fuse": fuse}
+
+
 def make_synth():
     out = []
     for ops, width, dens, devs, seed in ((490, 4, 0.5, (0, 1), 2312), (490, 4, 0.5, (0, 1), 1),
@@ -310,7 +420,7 @@ def make_synth():
 def main():
     jobs = {"schedules.json": make_schedules, "brute_force.json": make_brute, "gcof.json": make_gcof,
             "workload_evals.json": make_workload_evals, "synth.json": make_synth,
-            "solve_exact.json": make_solve_exact}
+            "solve_exact.json": make_solve_exact, "aux.json": make_aux}
     only = set(sys.argv[1:])
     for fname, fn in jobs.items():
         if only and fname not in only:
