@@ -11,6 +11,7 @@ tests/golden/*.json produced by tests/golden/make_golden.py).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from pathlib import Path
@@ -213,3 +214,53 @@ def cpu_count() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+# ---- K5 restated (paper_2312_04025_b200/csrc/mp_eval.cu mp_ls_kernel) -------------------
+_M64 = (1 << 64) - 1
+
+
+def _mix64(x: int) -> int:
+    x &= _M64
+    x ^= x >> 30
+    x = (x * 0xBF58476D1CE4E5B9) & _M64
+    x ^= x >> 27
+    x = (x * 0x94D049BB133111EB) & _M64
+    x ^= x >> 31
+    return x
+
+
+def ls_chains(orc: "OracleInstance", seeds, n_chains: int, chain_base: int, moves: int, rng_seed: int):
+    """CPU restatement of the local-search chains: chain c starts from seed row
+    (c % n_seed), move t re-assigns op (h mod n) to device (old + 1 + (h >> 32) mod
+    (K-1)) mod K with h = mix64(rng_seed ^ mix64(c * PHI + t)), accepted iff the
+    makespan does not increase (infeasible = +inf).  Exact only when no
+    evaluation overflows the GPU's ready capacity (the caller checks
+    ready_cap >= ready_bound).  Returns (best row, best ms, best chain, chain ms)."""
+    seeds = np.ascontiguousarray(seeds, np.uint8)
+    n, K = orc.n_ops, orc.K
+    chain_ms = np.empty(n_chains)
+    rows = []
+    for c in range(n_chains):
+        gc = c + chain_base
+        row = seeds[gc % len(seeds)].copy()
+
+        def ev(r):
+            st, ms, *_ = orc.schedule(r)
+            return ms if st == 0 else math.inf
+
+        cur = ev(row)
+        for t in range(moves if K > 1 else 0):
+            h = _mix64(rng_seed ^ _mix64(gc * 0x9E3779B97F4A7C15 + t))
+            i = (h & 0xFFFFFFFF) % n
+            old = int(row[i])
+            row[i] = (old + 1 + (h >> 32) % (K - 1)) % K
+            ms = ev(row)
+            if ms <= cur:
+                cur = ms
+            else:
+                row[i] = old
+        chain_ms[c] = cur
+        rows.append(row)
+    best = int(np.argmin(chain_ms)) if n_chains else 0
+    return rows[best], float(chain_ms[best]), best + chain_base, chain_ms

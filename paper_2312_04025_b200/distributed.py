@@ -81,3 +81,53 @@ def sharded_argmin(inst, rows_global: np.ndarray, rank: int, world: int, evaluat
     local_row, local_ms = evaluate(inst, rows_global[lo:hi]) if hi > lo else (-1, math.inf)
     global_row = lo + local_row if local_row >= 0 else -1
     return allgather_best(local_ms, global_row, group=group, device=device)
+
+
+def broadcast_row(row: np.ndarray, src: int, group=None, device=None) -> np.ndarray:
+    """Broadcast the winning placement row (n_ops bytes) from its owner rank."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(row, dtype=np.uint8).copy())
+    if device is not None:
+        t = t.to(device)
+    dist.broadcast(t, src=src, group=group)
+    return t.cpu().numpy()
+
+
+def distributed_local_search(inst, seeds: np.ndarray, *, rounds: int, chains: int, moves: int, seed: int,
+                             rank: int, world: int, group=None, device=None, search=None):
+    """K5 across GPUs: ``rounds`` rounds of ``chains`` chains in
+    total, sharded by contiguous global chain id.  Each round every rank runs its
+    chains (global ids ``[lo, hi)``, so proposals depend only on the global id),
+    the ranks all-gather a 16-byte ``(makespan bits, global chain)`` record, the
+    owner of the lexicographic minimum broadcasts its row, and the next round
+    starts every chain from that incumbent.  Results are independent of the world
+    size.  ``search(inst, seeds, chains, chain_base, moves, rng_seed) -> (row, ms,
+    chain)`` defaults to the GPU :func:`paper_2312_04025_b200.local_search`; the
+    CPU tests inject the oracle's restatement.  Returns ``(row, makespan)``."""
+    if search is None:
+        from .solver import local_search
+
+        def search(i, s, n, base, mv, rs):
+            row, ms, ch, _ = local_search(i, s, chains=n, moves=mv, seed=rs, chain_base=base)
+            return row, ms, ch
+
+    cur = np.ascontiguousarray(seeds, dtype=np.uint8)
+    best_row, best_ms = None, math.inf
+    for r in range(rounds):
+        lo, hi = shard_bounds(chains, rank, world)
+        if hi > lo:
+            row, ms, ch = search(inst, cur, hi - lo, lo, moves, seed + r)
+        else:
+            row, ms, ch = np.zeros(cur.shape[1], np.uint8), math.inf, -1
+        g_ms, g_ch = allgather_best(ms, ch if math.isfinite(ms) else -1, group=group, device=device)
+        if g_ch < 0:
+            break
+        owner = next(k for k in range(world) if shard_bounds(chains, k, world)[0] <= g_ch < shard_bounds(chains, k, world)[1])
+        win = broadcast_row(row if owner == rank else np.zeros(cur.shape[1], np.uint8), owner, group=group,
+                            device=device)
+        if g_ms <= best_ms:
+            best_row, best_ms = win, g_ms
+        cur = win.reshape(1, -1)
+    return best_row, best_ms

@@ -90,3 +90,66 @@ def test_sharded_argmin_gloo(world, oracle_mod):
     for p in procs:
         p.join(timeout=60)
     assert all(v == want for v in got.values()), (got, want)
+
+
+def _ls_instance():
+    rng = np.random.default_rng(11)
+    n, K = 10, 3
+    cost = rng.uniform(0.5, 8.0, (n, K)).round(3)
+    mem = rng.integers(1, 30, n)
+    src = np.array([j - 1 - (j % 3 == 0) for j in range(2, n)], dtype=np.int32)
+    dst = np.array(list(range(2, n)), dtype=np.int32)
+    src = np.concatenate([[0], src]).astype(np.int32)
+    dst = np.concatenate([[1], dst]).astype(np.int32)
+    pay = rng.integers(1_000_000, 30_000_000, len(src))
+    cap = np.array([150, 150, 150])
+    bw = rng.uniform(4e6, 4e7, (K, K))
+    return (cost, mem, src, dst, pay, cap, bw)
+
+
+def _ls_worker(rank, world, port, arrays, seeds, q):
+    import torch.distributed as dist
+
+    from oracle.oracle import OracleInstance, ls_chains
+    from paper_2312_04025_b200.distributed import distributed_local_search
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = OracleInstance(*arrays)
+
+    def search(_inst, s, n, base, moves, rs):  # CPU stand-in for the GPU chains
+        row, ms, ch, _ = ls_chains(orc, s, n, base, moves, rs)
+        return row, ms, ch
+
+    row, ms = distributed_local_search(None, seeds, rounds=3, chains=24, moves=6, seed=5, rank=rank, world=world,
+                                       search=search)
+    q.put((rank, (row.tolist(), ms)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_distributed_local_search_is_world_size_independent(world, oracle_mod):
+    """Per-round incumbent exchange (16 B all-gather + row broadcast): the result
+    equals the single-rank run of the same global chains."""
+    from oracle.oracle import OracleInstance, ls_chains
+
+    arrays = _ls_instance()
+    seeds = np.random.default_rng(2).integers(0, 3, (4, 10), dtype=np.uint8)
+    orc = OracleInstance(*arrays)
+    cur, best = seeds, math.inf
+    for r in range(3):  # the same rounds without any process group
+        row, ms, _, _ = ls_chains(orc, cur, 24, 0, 6, 5 + r)
+        best = min(best, ms)
+        cur = row.reshape(1, -1)
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ls_worker, args=(r, world, port, arrays, seeds, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v[1] == best for v in got.values()), (got, best)
+    assert all(v == got[0] for v in got.values())

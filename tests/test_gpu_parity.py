@@ -321,3 +321,28 @@ def test_local_search_reverifies_and_is_deterministic(oracle_mod):
         assert st == 0 and oms == a[1]
         assert a[1] <= seed_ms.min()
         assert a[1] == a[3].min()
+
+
+def test_local_search_trajectories_match_cpu_restatement(oracle_mod):
+    """Every chain's final makespan equals the CPU restatement of the chain
+    semantics (oracle.ls_chains) on instances whose ready capacity covers every
+    node (no overflow rejections), including a sharded chain base."""
+    from oracle.oracle import ls_chains
+
+    rng = random.Random(44)
+    checked = 0
+    for trial in range(8):
+        g, c = random_problem(rng, rng.randint(4, 12), rng.randint(2, 4), tight=trial % 2 == 1, ties=False,
+                              zero=False)
+        with mp.Instance(g, c, mp.effective_bandwidth(c)) as inst:
+            if inst.info()["ready_cap"] < inst.info()["ready_bound"]:
+                continue
+            orc = oracle_mod.OracleInstance.from_instance(inst)
+            seeds = np.random.default_rng(trial).integers(0, inst.K, (3, inst.n_ops), dtype=np.uint8)
+            for base in (0, 1000):
+                row, ms, ch, cms = mp.local_search(inst, seeds, chains=40, moves=12, seed=trial, chain_base=base)
+                wrow, wms, wch, wcms = ls_chains(orc, seeds, 40, base, 12, trial)
+                assert np.array_equal(bits(cms), bits(wcms)), (trial, base)
+                assert ch == wch and np.array_equal(row, wrow) and (ms == wms or math.isinf(wms))
+            checked += 1
+    assert checked >= 5
