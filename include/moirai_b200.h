@@ -227,6 +227,31 @@ int32_t mp_audit_schedule(mp_instance *inst, const uint8_t *row, const double *s
                           const double *ends, double tol, mp_violation *out, int64_t out_cap,
                           int64_t *n_out, mp_error *err);
 
+/* ---- graph ingestion (replaces the parse of fileio.load_graph, fileio.py:58-70) ----
+ * Streams a schema-1 graph document into flat arrays and applies the OpNode /
+ * FlowEdge / CompGraph validations (graph.py:31-109).  MP_ERR_INVALID (message in
+ * err) for anything off the fast path; the arrays live until mp_graph_doc_free.
+ * Strings (op types, type sequences) are interned: string k is
+ * str[str_beg[k] .. str_beg[k+1]) (UTF-8). */
+typedef struct mp_graph_doc mp_graph_doc;
+typedef struct mp_graph_view {
+    int64_t n_nodes, n_edges, n_strings;
+    const int64_t *id, *mem;            /* [n_nodes] in file order                       */
+    const int8_t *tag;                  /* [n_nodes] 0 plain, 1 fused, 2 bound           */
+    const int32_t *op_type;             /* [n_nodes] string index                        */
+    const int32_t *seq_beg, *seq;       /* type_seq: seq[seq_beg[i] .. seq_beg[i+1])    */
+    const int32_t *mem_beg;             /* members: members[mem_beg[i] .. mem_beg[i+1]) */
+    const int64_t *members;
+    const int32_t *ct_beg;              /* compute_time entries of node i, file order    */
+    const int64_t *ct_dev;
+    const double *ct_val;
+    const int64_t *esrc, *edst, *epay;  /* [n_edges] in file order                      */
+    const int64_t *str_beg;             /* [n_strings + 1]                               */
+    const char *str;
+} mp_graph_view;
+int32_t mp_graph_load_json(const char *path, mp_graph_doc **doc, mp_graph_view *view, mp_error *err);
+void    mp_graph_doc_free(mp_graph_doc *doc);
+
 /* ---- GCOF coarsening (K1/K2; replaces gcof, fusion.py:271-304) ----------- */
 typedef struct mp_coarsen_input {
     int32_t n_nodes;            /* V: input op nodes in ascending id order          */

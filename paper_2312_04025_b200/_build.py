@@ -20,7 +20,7 @@ ROOT = PKG.parent
 LIB = PKG / "libmoirai_b200.so"
 OBJ = PKG / "_obj"
 
-SOURCES = ["mp_eval.cu", "mp_instance.cu", "mp_bnb.cu", "mp_aux.cu", "mp_coarsen.cu"]
+SOURCES = ["mp_eval.cu", "mp_instance.cu", "mp_bnb.cu", "mp_aux.cu", "mp_coarsen.cu", "mp_io.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",
            "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     srcs = [CSRC / s for s in SOURCES if (CSRC / s).exists()]
     jobs = []
     for src in srcs:
-        obj = OBJ / (src.stem + ".o")
+        obj = OBJ / (src.stem + ".o")  # .cpp: host-only translation unit, same nvcc driver
         if force or _stale(obj, [src, *headers]):
             jobs.append([nvcc(), *ARCH, *NVFLAGS, "-c", str(src), "-o", str(obj)])
 

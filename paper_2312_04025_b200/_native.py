@@ -76,6 +76,16 @@ class mp_violation(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("x", C.c_int64), ("y", C.c_int64)]
 
 
+class mp_graph_view(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("n_edges", C.c_int64), ("n_strings", C.c_int64),
+                ("id", C.POINTER(C.c_int64)), ("mem", C.POINTER(C.c_int64)), ("tag", C.POINTER(C.c_int8)),
+                ("op_type", C.POINTER(C.c_int32)), ("seq_beg", C.POINTER(C.c_int32)), ("seq", C.POINTER(C.c_int32)),
+                ("mem_beg", C.POINTER(C.c_int32)), ("members", C.POINTER(C.c_int64)),
+                ("ct_beg", C.POINTER(C.c_int32)), ("ct_dev", C.POINTER(C.c_int64)), ("ct_val", C.POINTER(C.c_double)),
+                ("esrc", C.POINTER(C.c_int64)), ("edst", C.POINTER(C.c_int64)), ("epay", C.POINTER(C.c_int64)),
+                ("str_beg", C.POINTER(C.c_int64)), ("str", C.c_void_p)]
+
+
 class mp_coarsen_input(C.Structure):
     _fields_ = [
         ("n_nodes", C.c_int32), ("n_edges", C.c_int32), ("n_dev", C.c_int32),
@@ -131,6 +141,9 @@ SIGNATURES = {
     "mp_greedy_place": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(mp_error)]),
     "mp_audit_schedule": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                        C.c_int64, C.POINTER(C.c_int64), C.POINTER(mp_error)]),
+    "mp_graph_load_json": (C.c_int32, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(mp_graph_view),
+                                        C.POINTER(mp_error)]),
+    "mp_graph_doc_free": (None, [C.c_void_p]),
     "mp_coarsen": (C.c_int32, [C.POINTER(mp_coarsen_input), C.c_int32, C.POINTER(mp_coarsen_output),
                                C.POINTER(mp_error)]),
     "mp_coarsen_free": (None, [C.POINTER(mp_coarsen_output)]),
