@@ -346,3 +346,66 @@ def test_local_search_trajectories_match_cpu_restatement(oracle_mod):
                 assert ch == wch and np.array_equal(row, wrow) and (ms == wms or math.isinf(wms))
             checked += 1
     assert checked >= 5
+
+
+# ---- edge cases: sizes and shapes the reference accepts -------------------------------
+def _eval_vs_oracle(oracle_mod, g, c, rows):
+    with mp.Instance(g, c, mp.effective_bandwidth(c)) as inst:
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        want, wst = orc.eval_batch(rows)
+        for shape in (dict(), dict(group_lanes=32), dict(tpp=False), dict(tpp_smem=True)):
+            inst.tune(**shape)
+            ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
+            assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), shape
+        return inst.info()
+
+
+def test_edge_case_sizes(oracle_mod):
+    rng = np.random.default_rng(17)
+    one = mp.Cluster([mp.Device(0, 10 ** 9)], {})
+    # K = 1, a chain and an edgeless graph
+    chain = mp.CompGraph([mp.OpNode(i, "op", 1, {0: float(i)}) for i in range(1, 9)],
+                         [mp.FlowEdge(i, i + 1, 100) for i in range(1, 8)])
+    _eval_vs_oracle(oracle_mod, chain, one, np.zeros((5, 8), np.uint8))
+    flat = mp.CompGraph([mp.OpNode(i, "op", 1, {0: 1.0 + i % 3}) for i in range(1, 40)], [])
+    _eval_vs_oracle(oracle_mod, flat, one, np.zeros((3, 39), np.uint8))
+    # a single op on two devices
+    two = mp.Cluster([mp.Device(0, 5), mp.Device(1, 5)], {(0, 1): 1e6, (1, 0): 1e6})
+    single = mp.CompGraph([mp.OpNode(7, "op", 3, {0: 2.0, 1: 1.5})], [])
+    _eval_vs_oracle(oracle_mod, single, two, np.array([[0], [1]], np.uint8))
+    # 16 devices (the C ABI maximum), all-pairs bandwidths
+    k = 16
+    c16 = mp.Cluster([mp.Device(d, 10 ** 12) for d in range(k)],
+                     {(a, b): float(rng.uniform(1e6, 1e8)) for a in range(k) for b in range(k) if a != b})
+    g16 = mp.gen_synthetic(mp.GenSpec(ops=60, width=6, density=0.5, devices=tuple(range(k))), 4)
+    _eval_vs_oracle(oracle_mod, g16, c16, rng.integers(0, k, (400, len(g16)), dtype=np.uint8))
+    # empty batches and rows naming unknown devices
+    with mp.Instance(g16, c16, mp.effective_bandwidth(c16)) as inst:
+        assert len(mp.evaluate_batch(inst, np.zeros((0, len(g16)), np.uint8))) == 0
+        assert mp.argmin(inst, np.zeros((0, len(g16)), np.uint8)) == (-1, math.inf)
+        bad = rng.integers(0, k, (4, len(g16)), dtype=np.uint8)
+        bad[2, 5] = 200
+        ms, st, _, _ = mp.evaluate_batch(inst, bad, with_detail=True)
+        assert st.tolist()[2] == 2 and math.isinf(ms[2]) and (st != 2).sum() == 3
+
+
+def test_large_graph_and_batch_vs_oracle(oracle_mod):
+    """50k-op synthetic graph (coarsened on the GPU) and a 2^20-row batch through
+    the chunked host path: bit-exact against the oracle on samples."""
+    g = mp.gen_synthetic(mp.GenSpec(ops=50_000, width=32, density=0.5, devices=(0, 1, 2, 3)), 0)
+    coarse = mp.gcof(g, workloads.table_rules())
+    c = mp.Cluster([mp.Device(d, 10 ** 15) for d in range(4)],
+                   {(a, b): random.Random(0).uniform(4e6, 4e7) for a in range(4) for b in range(4) if a != b})
+    rows = np.random.default_rng(3).integers(0, 4, (24, len(coarse)), dtype=np.uint8)
+    _eval_vs_oracle(oracle_mod, coarse, c, rows)
+    w = workloads.c2(4)
+    c2 = mp.gcof(w.raw, w.rules)
+    with mp.Instance(c2, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        big = workloads.placements(77, 1 << 20, inst.n_ops, inst.K)
+        ms = mp.evaluate_batch(inst, big)
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        idx = np.random.default_rng(1).choice(len(big), 2000, replace=False)
+        want, _ = orc.eval_batch(big[idx], threads=8)
+        assert np.array_equal(bits(ms[idx]), bits(want))
+        best, bms = mp.argmin(inst, big)
+        assert bms == ms.min() and best == int(np.argmin(ms))
