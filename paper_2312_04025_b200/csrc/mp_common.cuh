@@ -99,7 +99,30 @@ struct EvalArgs {
     int row_list;                 // 1: `row_idx` lists the global rows to (re)evaluate
     const long long *row_idx;     // [n_rows] global row indices (row_list mode)
     long long lane_stride;        // TPP: lanes in the grid (stride of the lane-interleaved global state)
+    // streamed input (host rows copied while the kernel runs): rows [0, *rows_ready)
+    // have landed; null = all rows resident.  stream_fail is raised on a wait timeout.
+    const unsigned int *rows_ready;
+    unsigned int *stream_fail;
 };
+
+// Wait (lane 0 of a warp) until rows [.., need) of a streamed batch have landed.
+__device__ __forceinline__ void wait_rows(const EvalArgs &a, unsigned long long need) {
+    if (!a.rows_ready) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned int v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rows_ready) : "memory");
+        if (v >= need) return;
+        __nanosleep(512);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ULL) {  // 20 s: the copy never arrived; fail the call, do not hang
+            atomicExch(a.stream_fail, 1u);
+            return;
+        }
+    }
+}
 
 enum { SRC_LOAD = 0, SRC_ENUM = 1 };
 

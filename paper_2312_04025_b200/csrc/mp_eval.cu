@@ -504,7 +504,12 @@ __global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_eval_kernel(const __
 
     for (;;) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.next, static_cast<unsigned long long>(GPW));
+        if (lane == 0) {
+            base = atomicAdd(a.next, static_cast<unsigned long long>(GPW));
+            if constexpr (SRC == SRC_LOAD)
+                if (base < static_cast<unsigned long long>(n_rows))
+                    wait_rows(a, base + GPW < static_cast<unsigned long long>(n_rows) ? base + GPW : n_rows);
+        }
         base = __shfl_sync(kFull, base, 0);
         if (base >= static_cast<unsigned long long>(n_rows)) break;
         const unsigned long long p = base + static_cast<unsigned long long>(lane / G);
@@ -1346,7 +1351,11 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __g
     long long best_row = LLONG_MAX;
     for (;;) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.next, 32ULL);
+        if (lane == 0) {
+            base = atomicAdd(a.next, 32ULL);
+            if (base < static_cast<unsigned long long>(n_rows))
+                wait_rows(a, base + 32 < static_cast<unsigned long long>(n_rows) ? base + 32 : n_rows);
+        }
         base = __shfl_sync(kFull, base, 0);
         if (base >= static_cast<unsigned long long>(n_rows)) break;
         const unsigned long long p = base + lane;
@@ -1439,7 +1448,11 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
     long long best_row = LLONG_MAX;
     for (;;) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.next, 32ULL);
+        if (lane == 0) {
+            base = atomicAdd(a.next, 32ULL);
+            if (base < static_cast<unsigned long long>(n_rows))
+                wait_rows(a, base + 32 < static_cast<unsigned long long>(n_rows) ? base + 32 : n_rows);
+        }
         base = __shfl_sync(kFull, base, 0);
         if (base >= static_cast<unsigned long long>(n_rows)) break;
         const unsigned long long p = base + lane;

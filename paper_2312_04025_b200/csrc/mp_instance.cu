@@ -343,6 +343,11 @@ struct mp_instance {
     int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
     DevBuf tpp_state;
+    // streamed host input: a device word {rows ready, wait timeout} written by the copy
+    // stream with cuStreamWriteValue32 (driver entry point fetched at run time)
+    int stream_memop = 0;  // 0 unknown, 1 usable, -1 not available
+    void *write_value32 = nullptr;
+    DevBuf sflag;
     // per-call scratch
     DevBuf ctrs;      // [0] main next, [1] wide next, [2] ovf count (u32) ...
     DevBuf cta_best;  // ms[] then rows[]
@@ -948,10 +953,42 @@ long long *best_row_arr(mp_instance *I) {
                                          static_cast<size_t>(I->main.ctas + I->wide.ctas) * 8);
 }
 
+typedef int (*WriteValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+
+// Stream memory operations through the driver entry point (no link-time libcuda
+// dependency): probed once per instance with a write + read-back.
+bool stream_memop_ok(mp_instance *I) {
+    if (I->stream_memop != 0) return I->stream_memop > 0;
+    I->stream_memop = -1;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+        cudaGetLastError();
+        return false;
+    }
+    if (I->sflag.ensure(16) != cudaSuccess) return false;
+    unsigned int *flag = static_cast<unsigned int *>(I->sflag.p);
+    unsigned int h = 0;
+    if (cudaMemsetAsync(flag, 0, 8, I->stream) != cudaSuccess) return false;
+    if (reinterpret_cast<WriteValue32Fn>(fn)(I->stream, reinterpret_cast<unsigned long long>(flag), 0x5eedu, 0) != 0) {
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, I->stream) != cudaSuccess ||
+        cudaStreamSynchronize(I->stream) != cudaSuccess || h != 0x5eedu) {
+        cudaGetLastError();
+        return false;
+    }
+    I->write_value32 = fn;
+    I->stream_memop = 1;
+    return true;
+}
+
 // One evaluation pass over rows[0..n) (device pointers), outputs indexed from out_base.
 cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long row_base, long long out_base,
                      long long rows_bytes, double *ms, int8_t *st, int32_t *md, long long *ov, bool argmin,
-                     cudaStream_t s) {
+                     cudaStream_t s, const unsigned int *rows_ready = nullptr, cudaEvent_t rows_done = nullptr) {
     unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
     cudaError_t e = cudaMemsetAsync(ctr, 0, 64, s);
     if (e != cudaSuccess) return e;
@@ -971,6 +1008,8 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
     a.next = ctr;
     a.ovf_count = reinterpret_cast<unsigned int *>(ctr + 2);
     a.ovf_rows = static_cast<long long *>(I->ovf_rows.p);
+    a.rows_ready = rows_ready;
+    a.stream_fail = rows_ready ? const_cast<unsigned int *>(rows_ready) + 1 : nullptr;
     if (I->prefilter) {
         // memory check + compaction first; only feasible rows reach the scheduler
         unsigned int *nf = reinterpret_cast<unsigned int *>(ctr + 5);
@@ -992,6 +1031,7 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
     } else if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) {
         return e;
     }
+    if (rows_done && (e = cudaStreamWaitEvent(s, rows_done, 0)) != cudaSuccess) return e;
     if (first_rcap(I) < I->ready_bound) {
         // rows whose ready set outgrew the on-chip capacity: re-run off-chip
         EvalArgs b = base_args(I, true);
@@ -1049,9 +1089,48 @@ int evaluate_impl(mp_instance *I, const uint8_t *rows, long long n_rows, double 
         MP_CUDA(cudaGetLastError());
     }
     if (n_rows > 0) {
+        const bool stream_in = !devptr && !I->prefilter && n_rows >= 16LL * I->sms * 32 &&
+                               n_rows * row_bytes <= (4LL << 30) && stream_memop_ok(I);
         if (devptr) {
             MP_CUDA(run_rows(I, rows, n_rows, 0, 0, n_rows * row_bytes, makespan, status, mem_dev,
                              reinterpret_cast<long long *>(overflow), argmin, s));
+        } else if (stream_in) {
+            // host rows stream into the running kernel: the copy stream lands them in
+            // pieces and publishes "rows ready" after each; warps wait for their batch
+            MP_CUDA(I->rows_dev[0].ensure(static_cast<size_t>(n_rows * row_bytes + 64)));
+            MP_CUDA(I->out_dev[0].ensure(static_cast<size_t>(n_rows) * (8 + 1 + 4 + 8) + 64));
+            MP_CUDA(I->sflag.ensure(16));
+            unsigned int *flag = static_cast<unsigned int *>(I->sflag.p);
+            MP_CUDA(cudaMemsetAsync(flag, 0, 8, s));
+            MP_CUDA(cudaEventRecord(I->ev_used[0], s));
+            MP_CUDA(cudaStreamWaitEvent(I->copy_stream, I->ev_used[0], 0));
+            unsigned char *drows = static_cast<unsigned char *>(I->rows_dev[0].p);
+            // ~4 MB pieces: the first warps start after one small copy
+            const long long piece = std::max(1024LL, std::min(n_rows, (4LL << 20) / row_bytes));
+            auto wv = reinterpret_cast<WriteValue32Fn>(I->write_value32);
+            for (long long r0 = 0; r0 < n_rows; r0 += piece) {
+                const long long nr = std::min(piece, n_rows - r0);
+                MP_CUDA(cudaMemcpyAsync(drows + r0 * row_bytes, rows + r0 * row_bytes, static_cast<size_t>(nr * row_bytes),
+                                        cudaMemcpyHostToDevice, I->copy_stream));
+                if (wv(I->copy_stream, reinterpret_cast<unsigned long long>(flag), static_cast<unsigned int>(r0 + nr), 0) != 0)
+                    return set_err(err, MP_ERR_CUDA, 0, 0, "cuStreamWriteValue32 failed");
+            }
+            MP_CUDA(cudaEventRecord(I->ev_copy[0], I->copy_stream));
+            unsigned char *o = static_cast<unsigned char *>(I->out_dev[0].p);
+            double *dms = makespan ? reinterpret_cast<double *>(o) : nullptr;
+            long long *dov = overflow ? reinterpret_cast<long long *>(o + 8 * n_rows) : nullptr;
+            int32_t *dmd = mem_dev ? reinterpret_cast<int32_t *>(o + 16 * n_rows) : nullptr;
+            int8_t *dst = status ? reinterpret_cast<int8_t *>(o + 20 * n_rows) : nullptr;
+            MP_CUDA(run_rows(I, drows, n_rows, 0, 0, n_rows * row_bytes, dms, dst, dmd, dov, argmin, s, flag,
+                             I->ev_copy[0]));
+            if (makespan) MP_CUDA(cudaMemcpyAsync(makespan, dms, 8 * n_rows, cudaMemcpyDeviceToHost, s));
+            if (overflow) MP_CUDA(cudaMemcpyAsync(overflow, dov, 8 * n_rows, cudaMemcpyDeviceToHost, s));
+            if (mem_dev) MP_CUDA(cudaMemcpyAsync(mem_dev, dmd, 4 * n_rows, cudaMemcpyDeviceToHost, s));
+            if (status) MP_CUDA(cudaMemcpyAsync(status, dst, n_rows, cudaMemcpyDeviceToHost, s));
+            unsigned int hflag[2] = {0, 0};
+            MP_CUDA(cudaMemcpyAsync(hflag, flag, 8, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+            if (hflag[1]) return set_err(err, MP_ERR_CUDA, 0, 0, "streamed rows did not arrive within 20 s");
         } else {
             // host buffers: double-buffered chunks, H2D on the copy stream
             // overlapping the evaluation of the previous chunk.
