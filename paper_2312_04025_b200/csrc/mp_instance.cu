@@ -339,7 +339,8 @@ struct mp_instance {
     DevBuf main_state, wide_state;
     // thread-per-placement variant (mp_tpp_kernel); tpp_rc == 0: not used
     bool tpp_allowed = true;
-    bool tpp_smem_pref = false;  // MP_TUNE_TPP_SMEM: shared-memory ready set even when registers fit
+    bool tpp_smem_pref = false;
+    bool force_offchip = false;  // MP_TUNE_OFFCHIP  // MP_TUNE_TPP_SMEM: shared-memory ready set even when registers fit
     int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
     DevBuf tpp_state;
@@ -441,13 +442,27 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     w.ctas = static_cast<int>(std::max(1LL, groups / 8));
     I->wide = w;
     I->wide_so = wso;
-    if (!(mode > 0 && best_w >= 1)) {
-        // huge instance: state in global memory too, capacity from the probe
+    // Off-chip main variant (state slices in global memory, L2-resident): used when
+    // nothing fits on chip, when the caller forces it, or when the on-chip shape keeps
+    // fewer than 16 placements in flight per SM — measured on C5 (ready sets of
+    // 100-200): 8-lane groups, 32 per CTA off-chip run 1.5x faster than 14 on-chip
+    // 32-lane groups (profiles/r01/c5_shapes.txt).
+    const long long onchip_per_sm = (mode > 0 && best_w >= 1)
+                                        ? static_cast<long long>(I->main.groups_per_cta) * (I->main.ctas / std::max(1, I->sms))
+                                        : 0;
+    const bool off = !(mode > 0 && best_w >= 1) || I->force_offchip ||
+                     (G_req == 0 && U_req == 0 && onchip_per_sm < 16 && I->peak_probe >= 0);
+    if (off) {
         LaunchShape m = w;
-        m.G = G_req > 0 ? G_req : 32;
+        // lanes per placement from the calibrated ready-set peak: ~30-75 entries per
+        // lane per scan (measured: peak 222 -> G 8, 376/874 -> G 16, c5_shapes.txt)
+        const int pk = I->peak_probe > 0 ? I->peak_probe : I->ready_bound;
+        m.G = G_req > 0 ? G_req : (pk <= 300 ? 8 : (pk <= 1200 ? 16 : 32));
         m.U = 32;
-        m.groups_per_cta = 8 * (32 / m.G);
-        long long g2 = static_cast<long long>(I->sms) * m.groups_per_cta;
+        m.threads = 256;
+        m.groups_per_cta = (m.threads / 32) * (32 / m.G);
+        const int per_sm = ctas_per_sm_req > 0 ? ctas_per_sm_req : 2;
+        long long g2 = static_cast<long long>(I->sms) * per_sm * m.groups_per_cta;
         while (g2 > m.groups_per_cta && g2 * static_cast<long long>(so.bytes) > budget) g2 /= 2;
         m.ctas = static_cast<int>(std::max(1LL, g2 / m.groups_per_cta));
         I->main = m;
@@ -889,6 +904,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
     I->tpp_smem_pref = (flags & MP_TUNE_TPP_SMEM) != 0;
+    I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }

@@ -215,7 +215,9 @@ def random_problem(rng, n_ops, k, tight=False, ties=False, zero=False):
 
 SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (1, 2, 4, 8, 16, 32) for colo in (True, False)
           for rc in (0, 3)] + [dict(group_lanes=1, lanes_used=8), dict(group_lanes=2, lanes_used=16),
-                               dict(group_lanes=4, lanes_used=8, ready_cap=2)]
+                               dict(group_lanes=4, lanes_used=8, ready_cap=2),
+                               dict(offchip=True), dict(offchip=True, group_lanes=4, ready_cap=3),
+                               dict(offchip=True, group_lanes=32, colo=False)]
 # automatic shape -> the thread-per-placement kernel when the calibrated ready set
 # fits its register capacity (4 / 8 / 16 entries; ready_cap=3 forces reruns)
 TPP_SHAPES = [dict(), dict(colo=False), dict(ready_cap=3), dict(ready_cap=6, colo=False), dict(ready_cap=12),
