@@ -112,7 +112,11 @@ __device__ __forceinline__ void wait_rows(const EvalArgs &a, unsigned long long 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         unsigned int v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rows_ready) : "memory");
+        // relaxed poll: an acquire load here would invalidate the SM's L1 on every batch.
+        // The rows themselves are read with L2-only loads (ld.global.cg), so lines
+        // cached before a piece landed are never served, and no load is issued
+        // before this loop exits (no speculation across the branch).
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rows_ready) : "memory");
         if (v >= need) return;
         __nanosleep(512);
         unsigned long long t;

@@ -71,7 +71,7 @@ __device__ __forceinline__ int load_row(unsigned char *buf, const uint8_t *rows,
         const long long off = a0 + 16LL * c;
         uint4 v;
         if (off + 16 <= rows_bytes) {
-            v = __ldcs(reinterpret_cast<const uint4 *>(rows + off));
+            v = __ldcg(reinterpret_cast<const uint4 *>(rows + off));
         } else {
             uint32_t w[4] = {0, 0, 0, 0};
             for (int b = 0; b < 16; ++b)
@@ -798,7 +798,7 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
         const long long off = a0 + 16LL * c;
         uint4 w;
         if (off + 16 <= rows_bytes) {
-            w = __ldcs(reinterpret_cast<const uint4 *>(rows + off));
+            w = __ldcg(reinterpret_cast<const uint4 *>(rows + off));
         } else {
             uint32_t x[4] = {0, 0, 0, 0};
             for (int b = 0; b < 16; ++b)

@@ -11,10 +11,13 @@
 
 #include <cub/cub.cuh>
 
+#include <functional>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -1004,7 +1007,8 @@ bool stream_memop_ok(mp_instance *I) {
 // One evaluation pass over rows[0..n) (device pointers), outputs indexed from out_base.
 cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long row_base, long long out_base,
                      long long rows_bytes, double *ms, int8_t *st, int32_t *md, long long *ov, bool argmin,
-                     cudaStream_t s, const unsigned int *rows_ready = nullptr, cudaEvent_t rows_done = nullptr) {
+                     cudaStream_t s, const unsigned int *rows_ready = nullptr, cudaEvent_t rows_done = nullptr,
+                     const std::function<cudaError_t()> &after_main = nullptr) {
     unsigned long long *ctr = static_cast<unsigned long long *>(I->ctrs.p);
     cudaError_t e = cudaMemsetAsync(ctr, 0, 64, s);
     if (e != cudaSuccess) return e;
@@ -1047,6 +1051,9 @@ cudaError_t run_rows(mp_instance *I, const uint8_t *rows, long long n, long long
     } else if ((e = mp_launch_eval(I->main, SRC_LOAD, false, a, s)) != cudaSuccess) {
         return e;
     }
+    // streamed input: the copies are enqueued only now, so the kernel is already
+    // resident (and waiting) when the first piece lands
+    if (after_main && (e = after_main()) != cudaSuccess) return e;
     if (rows_done && (e = cudaStreamWaitEvent(s, rows_done, 0)) != cudaSuccess) return e;
     if (first_rcap(I) < I->ready_bound) {
         // rows whose ready set outgrew the on-chip capacity: re-run off-chip
@@ -1121,24 +1128,40 @@ int evaluate_impl(mp_instance *I, const uint8_t *rows, long long n_rows, double 
             MP_CUDA(cudaEventRecord(I->ev_used[0], s));
             MP_CUDA(cudaStreamWaitEvent(I->copy_stream, I->ev_used[0], 0));
             unsigned char *drows = static_cast<unsigned char *>(I->rows_dev[0].p);
-            // ~4 MB pieces: the first warps start after one small copy
-            const long long piece = std::max(1024LL, std::min(n_rows, (4LL << 20) / row_bytes));
+            // pieces grow from 2 MB (the first warps start early) to 32 MB (few API calls)
             auto wv = reinterpret_cast<WriteValue32Fn>(I->write_value32);
-            for (long long r0 = 0; r0 < n_rows; r0 += piece) {
-                const long long nr = std::min(piece, n_rows - r0);
-                MP_CUDA(cudaMemcpyAsync(drows + r0 * row_bytes, rows + r0 * row_bytes, static_cast<size_t>(nr * row_bytes),
-                                        cudaMemcpyHostToDevice, I->copy_stream));
-                if (wv(I->copy_stream, reinterpret_cast<unsigned long long>(flag), static_cast<unsigned int>(r0 + nr), 0) != 0)
-                    return set_err(err, MP_ERR_CUDA, 0, 0, "cuStreamWriteValue32 failed");
-            }
-            MP_CUDA(cudaEventRecord(I->ev_copy[0], I->copy_stream));
+            bool wv_fail = false;
+            auto enqueue_copies = [&]() -> cudaError_t {
+                long long r0 = 0;
+                long long piece = std::max(1024LL, (2LL << 20) / row_bytes);
+                const long long max_piece = std::max(1024LL, (32LL << 20) / row_bytes);
+                while (r0 < n_rows) {
+                    const long long nr = std::min(piece, n_rows - r0);
+                    cudaError_t ce = cudaMemcpyAsync(drows + r0 * row_bytes, rows + r0 * row_bytes,
+                                                     static_cast<size_t>(nr * row_bytes), cudaMemcpyHostToDevice,
+                                                     I->copy_stream);
+                    if (ce != cudaSuccess) return ce;
+                    if (wv(I->copy_stream, reinterpret_cast<unsigned long long>(flag), static_cast<unsigned int>(r0 + nr),
+                           0) != 0) {
+                        wv_fail = true;
+                        return cudaErrorUnknown;
+                    }
+                    r0 += nr;
+                    piece = std::min(max_piece, 2 * piece);
+                }
+                return cudaEventRecord(I->ev_copy[0], I->copy_stream);
+            };
             unsigned char *o = static_cast<unsigned char *>(I->out_dev[0].p);
             double *dms = makespan ? reinterpret_cast<double *>(o) : nullptr;
             long long *dov = overflow ? reinterpret_cast<long long *>(o + 8 * n_rows) : nullptr;
             int32_t *dmd = mem_dev ? reinterpret_cast<int32_t *>(o + 16 * n_rows) : nullptr;
             int8_t *dst = status ? reinterpret_cast<int8_t *>(o + 20 * n_rows) : nullptr;
-            MP_CUDA(run_rows(I, drows, n_rows, 0, 0, n_rows * row_bytes, dms, dst, dmd, dov, argmin, s, flag,
-                             I->ev_copy[0]));
+            {
+                const cudaError_t re = run_rows(I, drows, n_rows, 0, 0, n_rows * row_bytes, dms, dst, dmd, dov, argmin,
+                                                s, flag, I->ev_copy[0], enqueue_copies);
+                if (wv_fail) return set_err(err, MP_ERR_CUDA, 0, 0, "cuStreamWriteValue32 failed");
+                MP_CUDA(re);
+            }
             if (makespan) MP_CUDA(cudaMemcpyAsync(makespan, dms, 8 * n_rows, cudaMemcpyDeviceToHost, s));
             if (overflow) MP_CUDA(cudaMemcpyAsync(overflow, dov, 8 * n_rows, cudaMemcpyDeviceToHost, s));
             if (mem_dev) MP_CUDA(cudaMemcpyAsync(mem_dev, dmd, 4 * n_rows, cudaMemcpyDeviceToHost, s));
