@@ -39,6 +39,8 @@ def test_struct_layouts_match_header():
     assert C.sizeof(N.mp_problem) == 16 + 7 * 8
     # 21 int32 (+ pad) + 2 int64 + 3 int32 (tpp_ready_cap, tpp_threads, tpp_kind) + tail pad
     assert C.sizeof(N.mp_instance_info) == 22 * 4 + 2 * 8 + 4 * 4
+    assert C.sizeof(N.mp_violation) == 4 + 4 + 8 + 8
+    assert C.sizeof(N.mp_graph_view) == 3 * 8 + 16 * 8
 
 
 def _no_gpu():
