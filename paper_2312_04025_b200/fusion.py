@@ -241,8 +241,8 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         new_nodes.append(_make_opnode(gid, FUSE_JOINER.join(seq), int(gmem[z]), cost, mids, seq,
                                       _CODE_TAG[int(grp_tag[z])]))
         gid_of.append(gid)
-    edges = [_make_edge(gid_of[u], gid_of[v], p) for u, v, p in zip(esrc.tolist(), edst.tolist(), epay.tolist())]
-    return CompGraph._trusted(new_nodes, edges)
+    # output nodes come in ascending id order, so group indices are node indices
+    return CompGraph._from_arrays(new_nodes, esrc, edst, epay)
 
 
 def _combined_cost(parts, seq, overrides):
