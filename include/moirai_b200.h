@@ -108,6 +108,7 @@ typedef struct mp_instance_info {
     int32_t tpp_ready_cap;      /* >0: thread-per-placement kernel in use, register ready capacity */
     int32_t tpp_threads;        /* placements per CTA of the thread-per-placement kernel */
     int32_t tpp_kind;           /* 1: ready set in registers, 2: in shared memory            */
+    int32_t ls_ready_cap;       /* local search: proposals whose ready set exceeds it are rejected */
 } mp_instance_info;
 
 /* ---- library ------------------------------------------------------------ */

@@ -337,6 +337,7 @@ struct mp_instance {
     LaunchShape main{};
     StOff main_so{};
     int main_rcap = 0;
+    int ls_cap = 0;    // local-search ready capacity, the same for every kernel (results never depend on the shape)
     LaunchShape wide{};
     StOff wide_so{};
     DevBuf main_state, wide_state;
@@ -365,6 +366,8 @@ struct mp_instance {
 };
 
 namespace {
+
+void set_ls_cap(mp_instance *I, int ready_cap_req);
 
 void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, int ready_cap_req = 0) {
     const int n_ops = I->n_ops, K = I->K;
@@ -506,6 +509,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         }
         I->tpp_ctas = std::min(I->sms, I->main.ctas);
     }
+    set_ls_cap(I, ready_cap_req);
 }
 
 // thread-per-placement shape with a shared-memory ready set of capacity `cap`
@@ -517,6 +521,16 @@ void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
     *threads = T >= 64 ? T : 0;
     *smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(I->n_ops) * T + 15) & ~15LL) + per_lane * T -
                              static_cast<long long>(I->n_ops) * T);
+}
+
+// Local search rejects a proposal whose ready set exceeds ls_cap in every kernel,
+// so chains are identical whichever kernel runs them: the calibrated peak (>= 4),
+// within what the group kernel's slots hold.
+// An explicit ready_cap (mp_instance_tune) sets it instead.
+void set_ls_cap(mp_instance *I, int ready_cap_req) {
+    const int pk = I->peak_probe > 0 ? I->peak_probe : I->main_rcap;
+    const int want = ready_cap_req > 0 ? ready_cap_req : std::max(4, pk);
+    I->ls_cap = std::max(1, std::min(I->main_rcap, std::min(I->ready_bound, want)));
 }
 
 // ready capacity of the variant that runs first (rows beyond it re-run off-chip)
@@ -888,6 +902,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->state_bytes = I->main_so.bytes;
     info->tpp_ready_cap = I->tpp_rc;
     info->tpp_kind = I->tpp_kind;
+    info->ls_ready_cap = I->ls_cap;
     info->tpp_threads = I->tpp_rc > 0 ? I->tpp_threads : 0;
     return MP_OK;
 }
@@ -1425,11 +1440,12 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     ls.rng_seed = rng_seed;
     ls.chain_rows = drows;
     ls.chain_ms = dms;
-    // thread-per-placement chains when the instance has a TPP shape and the group
-    // kernel's capacity fits a register template (same capacity -> same results)
-    const int ls_rc = I->main_rcap <= 4 ? 4 : (I->main_rcap <= 8 ? 8 : (I->main_rcap <= 16 ? 16 : 0));
+    // thread-per-placement chains when the instance has a TPP shape and the LS
+    // capacity fits a register template (same capacity in every kernel -> same results)
+    a.rcap = I->ls_cap;
+    const int ls_rc = I->ls_cap <= 4 ? 4 : (I->ls_cap <= 8 ? 8 : (I->ls_cap <= 16 ? 16 : 0));
     int ls_T = 0, ls_smem = 0;
-    if (I->tpp_kind == 2) tpps_shape(I, I->main_rcap, &ls_T, &ls_smem);
+    if (I->tpp_kind == 2) tpps_shape(I, I->ls_cap, &ls_T, &ls_smem);
     if (I->tpp_kind == 2 && ls_T > 0) {
         MP_CUDA(I->tpp_state.ensure(mp_tpp_state_bytes(I->n_ops, I->n_multi, static_cast<long long>(I->tpp_ctas) * ls_T)));
         a.lane_stride = static_cast<long long>(I->tpp_ctas) * ls_T;

@@ -337,7 +337,8 @@ def test_local_search_trajectories_match_cpu_restatement(oracle_mod):
         g, c = random_problem(rng, rng.randint(4, 12), rng.randint(2, 4), tight=trial % 2 == 1, ties=False,
                               zero=False)
         with mp.Instance(g, c, mp.effective_bandwidth(c)) as inst:
-            if inst.info()["ready_cap"] < inst.info()["ready_bound"]:
+            inst.tune(ready_cap=inst.info()["ready_bound"])  # no proposal can overflow
+            if inst.info()["ls_ready_cap"] < inst.info()["ready_bound"]:
                 continue
             orc = oracle_mod.OracleInstance.from_instance(inst)
             seeds = np.random.default_rng(trial).integers(0, inst.K, (3, inst.n_ops), dtype=np.uint8)
