@@ -236,8 +236,20 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # under torchrun the NCCL group is always formed (also at N=1, so the collective
+    # path is the one timed on every N)
+    use_dist = world > 1 or "MASTER_ADDR" in os.environ
+    if use_dist:
+        # NCCL prints its version banner on stdout from C; keep stdout for the one JSON line
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     w = build_workload(args.workload)
     t0 = time.perf_counter()
     coarse = mp.gcof(w.raw, w.rules, device=local)
@@ -270,7 +282,7 @@ def run_ours(args):
         all-gathered over NCCL, lexicographic minimum (paper_2312_04025_b200.distributed)."""
         rec = encode_record(bms.value, best.value + rank * P if best.value >= 0 else -1)
         gather_in.copy_(torch.from_numpy(rec), non_blocking=True)
-        if world > 1:
+        if use_dist:
             dist.all_gather_into_tensor(gather_out, gather_in)
             return combine_records(gather_out.cpu().numpy())
         return combine_records(gather_in.cpu().numpy())
@@ -290,12 +302,12 @@ def run_ours(args):
         return exchange()
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -396,7 +408,7 @@ def run_ours(args):
             arrays = inst._arrays
             out["cpu_baseline"] = cpu_baseline_python(arrays, rows, args.cpu_seconds)
             out["cpu_baseline_native"] = cpu_baseline_native(arrays, rows, args.cpu_seconds / 3)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     inst.close()
