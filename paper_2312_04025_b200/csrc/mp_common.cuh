@@ -36,6 +36,7 @@ struct TabOff {
     uint32_t lvl_ops;   // u32 [n_ops]      ops bucketed by height (0 = sinks)
     uint32_t lvl_beg;   // u32 [n_ops+1]    level offsets into lvl_ops
     uint32_t srcs;      // u32 [n_ops]      ops with no in-flow (initial ready set, solver.py:111)
+    uint32_t fpay;      // f64 [n_flows]    payload by flow index (durations recomputed at commit)
     uint32_t bytes;     // total, multiple of 16
 };
 

@@ -739,19 +739,23 @@ struct TppView {
     const uint32_t *T_out_beg, *T_fdst, *T_mi, *T_lvl, *T_srcs, *T_mdeg, *T_mop;
     int fast;
     uint32_t RZ, WS;
-    // shared-memory ready set (tpps_eval): [cap][T] each, dense per lane
+    // shared-memory ready set (tpps_eval): [cap][T] each, dense per lane; the
+    // duration is recomputed for the winner only
     unsigned long long *rE, *rR, *rM;  // est bits, rank bits, meta | tie << 32
-    double *rD;                        // duration
+    const double *T_fpay;              // payload by flow index
 };
 
-__device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm) {
+// nib: the row tile holds two device indices per byte (shared-memory ready-set
+// variant, K <= 16), (n_ops + 1) / 2 bytes per lane
+__device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm, bool nib = false) {
     TppView v;
     v.T = blockDim.x;
     v.tid = threadIdx.x;
     v.n_ops = a.n_ops;
     v.K = a.K;
     v.rowt = sm + a.to.bytes;
-    v.clk = reinterpret_cast<double *>(sm + a.to.bytes + ((static_cast<size_t>(a.n_ops) * v.T + 15) & ~static_cast<size_t>(15)));
+    const size_t row_bytes = nib ? static_cast<size_t>((a.n_ops + 1) / 2) : static_cast<size_t>(a.n_ops);
+    v.clk = reinterpret_cast<double *>(sm + a.to.bytes + ((row_bytes * v.T + 15) & ~static_cast<size_t>(15)));
     v.ld = reinterpret_cast<unsigned long long *>(v.clk);
     v.L = a.lane_stride;
     const long long gl = static_cast<long long>(blockIdx.x) * v.T + v.tid;
@@ -781,12 +785,14 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.rE = reinterpret_cast<unsigned long long *>(v.clk + static_cast<size_t>(3 * a.K + 2) * v.T);
     v.rR = v.rE + rdy;
     v.rM = v.rR + rdy;
-    v.rD = reinterpret_cast<double *>(v.rM + rdy);
+    v.T_fpay = tab<double>(tb, a.to.fpay);
     return v;
 }
 
 // Load one placement row (global byte offset `start`) into this lane's column of
-// the row tile with 16-byte streaming loads; returns true if it names a device >= K.
+// the row tile with 16-byte L2 loads; returns true if it names a device >= K.
+// NIB: pack two device indices per byte (low nibble = even op).
+template <bool NIB = false>
 __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *rows, long long rows_bytes,
                                              long long start, bool live) {
     bool bad = false;
@@ -812,12 +818,19 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
             if (pos >= 0 && pos < n_ops) {
                 const unsigned char d = static_cast<unsigned char>(w4[b >> 2] >> (8 * (b & 3)));
                 bad |= d >= v.K;
-                v.rowt[pos * T + tid] = d;
+                if constexpr (NIB) {
+                    unsigned char *cell = &v.rowt[(pos >> 1) * T + tid];
+                    *cell = (pos & 1) ? static_cast<unsigned char>((*cell & 0x0Fu) | ((d & 15u) << 4))
+                                      : static_cast<unsigned char>(d & 15u);
+                } else {
+                    v.rowt[pos * T + tid] = d;
+                }
             }
         }
     }
-    if (!live || bad) {
-        for (int i = 0; i < n_ops; ++i) v.rowt[i * T + tid] = 0;  // keep the lockstep passes in bounds
+    if (!live || bad) {  // keep the lockstep passes in bounds
+        const int nb = NIB ? (n_ops + 1) / 2 : n_ops;
+        for (int i = 0; i < nb; ++i) v.rowt[i * T + tid] = 0;
     }
     return bad;
 }
@@ -1116,7 +1129,9 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
     const int fast = v.fast;
     const uint32_t RZ = v.RZ, WS = v.WS;
     unsigned long long *rE = v.rE, *rR = v.rR, *rM = v.rM;
-    double *rD = v.rD;
+    const double *__restrict__ T_fpay = v.T_fpay;
+    // device index of op x from the nibble-packed row tile
+    auto dev = [&](int x) -> int { return (rowt[(x >> 1) * T + tid] >> ((x & 1) << 2)) & 15; };
     TppResult r;
     // ---- 1. memory feasibility (solver.py:82-87) ------------------------------------
     int status = bad ? MP_ROW_BAD_DEVICE : MP_ROW_OK;
@@ -1125,7 +1140,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
     for (int k = 0; k < K; ++k) ld[k * T + tid] = 0ULL;
     if (live && !bad) {
         for (int i = 0; i < n_ops; ++i) {
-            const int d = rowt[i * T + tid];
+            const int d = dev(i);
             ld[d * T + tid] += static_cast<unsigned long long>(T_mem[i]);
         }
         for (int k = 0; k < K; ++k) {
@@ -1144,13 +1159,13 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
     // ---- 2+3. durations + rank, ops in ascending height (solver.py:89-107) -----------
     for (int t = 0; t < n_ops; ++t) {
         const int i = static_cast<int>(T_lvl[t]);
-        const int d = rowt[i * T + tid];
+        const int d = dev(i);
         double best = 0.0;
         const int qe = static_cast<int>(T_out_beg[i + 1]);
         for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
             const double2 rec = T_rec[q];
             const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
-            const int dj = rowt[j * T + tid];
+            const int dj = dev(j);
             const bool cross = dj != d;
             const int bi = cross ? d * K + dj : 0;
             const double dv = div_bw(rec.y, cross ? T_bw[bi] : 1.0, cross ? T_rbw[bi] : 1.0, fast);
@@ -1178,7 +1193,6 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
             const int o = nr * T + tid;
             rE[o] = est;
             rR[o] = rk;
-            rD[o] = du;
             rM[o] = static_cast<unsigned long long>(meta) | (static_cast<unsigned long long>(tie) << 32);
         }
         nr += (ins && room) ? 1 : 0;
@@ -1186,7 +1200,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
     if (alive) {
         for (int t = 0; t < a.n_src; ++t) {
             const int i = static_cast<int>(T_srcs[t]);
-            const int d = rowt[i * T + tid];
+            const int d = dev(i);
             insert(true, 0ULL, dbits(g_rank[static_cast<long long>(i) * L]), T_cost[i * K + d],
                    static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26), static_cast<uint32_t>(i));
         }
@@ -1219,7 +1233,19 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
             bm = take ? m : bm;
             bs = take ? s : bs;
         }
-        const double bd = done ? 0.0 : rD[bs * T + tid];
+        // the winner's duration (not stored): op cost, payload / bw for a crossing
+        // flow, 0 for a co-located flow dispatched as a node (colo off)
+        double bd = 0.0;
+        {
+            const int wn = static_cast<int>(bm & MP_NODE_MASK);
+            const uint32_t w1 = (bm >> 20) & 63u, w2 = bm >> 26;
+            if (!done && wn < n_ops) {
+                bd = T_cost[wn * K + static_cast<int>(w1)];
+            } else if (!done && w1 != RZ) {
+                const int ka = static_cast<int>(w1) - K, kb = static_cast<int>(w2) - 2 * K;
+                bd = div_bw(T_fpay[wn - n_ops], T_bw[ka * K + kb], T_rbw[ka * K + kb], fast);
+            }
+        }
         // unordered removal: the last entry moves into the hole
         const int last = nr - 1;
         if (!done && bs != last) {
@@ -1227,7 +1253,6 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
             rE[o] = rE[ol];
             rR[o] = rR[ol];
             rM[o] = rM[ol];
-            rD[o] = rD[ol];
         }
         nr = done ? nr : last;
         // -- commit (solver.py:130-138) ------------------------------------------------
@@ -1269,7 +1294,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
                 const unsigned long long rb = dbits(rec.x);
                 const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
                 j_[u] = j;
-                dj_[u] = rowt[j * T + tid];
+                dj_[u] = dev(j);
                 pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
                 pay_[u] = rec.y;
                 act_[u] = act;
@@ -1442,7 +1467,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
     __shared__ long long s_best_row[MP_TPP_MAX_THREADS / 32];
     const int lane = threadIdx.x & 31;
     stage_tables(sm, a, &s_bar);
-    const TppView v = tpp_view(a, sm);
+    const TppView v = tpp_view(a, sm, true);
     const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
     double best_ms = kInf;
     long long best_row = LLONG_MAX;
@@ -1459,7 +1484,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
         const bool live = p < static_cast<unsigned long long>(n_rows);
         const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
         const long long grow = a.row_base + lrow;
-        const bool bad = tpp_load_row(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
+        const bool bad = tpp_load_row<true>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
         const TppResult r = tpps_eval<COLO>(v, a, live, bad, a.rcap);
         if (live) {
             const long long o = grow - a.out_base;
@@ -1494,7 +1519,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
     __shared__ __align__(8) uint64_t s_bar;
     const int lane = threadIdx.x & 31;
     stage_tables(sm, a, &s_bar);
-    const TppView v = tpp_view(a, sm);
+    const TppView v = tpp_view(a, sm, true);
     const int n = a.n_ops, K = a.K, T = v.T, tid = v.tid;
     for (;;) {
         unsigned long long base = 0;
@@ -1505,25 +1530,27 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
         const bool live = c < static_cast<unsigned long long>(ls.n_chains);
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
         const long long srow = live ? static_cast<long long>(gc % static_cast<unsigned long long>(ls.n_seed)) : 0;
-        tpp_load_row(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
+        tpp_load_row<true>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
         const TppResult r0 = tpps_eval<COLO>(v, a, live, false, a.rcap);
         double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
             const int i = static_cast<int>((h & 0xffffffffULL) % static_cast<unsigned long long>(n));
-            const int old = v.rowt[i * T + tid];
+            unsigned char *cell = &v.rowt[(i >> 1) * T + tid];
+            const int sh = (i & 1) << 2;
+            const int old = (*cell >> sh) & 15;
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
-            if (live) v.rowt[i * T + tid] = static_cast<unsigned char>(nd);
+            if (live) *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (nd << sh));
             const TppResult r = tpps_eval<COLO>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
                 cur_ms = ms;
             } else if (live) {
-                v.rowt[i * T + tid] = static_cast<unsigned char>(old);
+                *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (old << sh));
             }
         }
         if (live) {
-            for (int i = 0; i < n; ++i) ls.chain_rows[c * n + i] = v.rowt[i * T + tid];
+            for (int i = 0; i < n; ++i) ls.chain_rows[c * n + i] = (v.rowt[(i >> 1) * T + tid] >> ((i & 1) << 2)) & 15;
             ls.chain_ms[c] = cur_ms;
         }
         __syncwarp();

@@ -107,6 +107,7 @@ __global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cos
         const int s = fsrc[f], d = fdst[f];
         // Python int -> float conversion is correctly rounded, as is this cast.
         pay_d[f] = static_cast<double>(payload[f]);
+        reinterpret_cast<double *>(blob + to.fpay)[f] = pay_d[f];
         atomicMin(&be->min_payload, payload[f]);
         if (s < 0 || s >= n_ops || d < 0 || d >= n_ops || s == d) {
             atomicMin(&be->bad_flow, static_cast<unsigned long long>(f));
@@ -295,6 +296,7 @@ TabOff make_taboff(int n_ops, int n_flows, int K) {
     t.lvl_ops = take(4ULL * n_ops);
     t.lvl_beg = take(4ULL * (n_ops + 1));
     t.srcs = take(4ULL * n_ops);
+    t.fpay = take(8ULL * n_flows);
     t.bytes = static_cast<uint32_t>(o);
     return t;
 }
@@ -483,10 +485,11 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
         const long long avail = static_cast<long long>(smem_cap) - I->to.bytes - 32;
         const long long base_lane = n_ops + 8LL * (3 * K + 2);
-        // shared-memory ready set: 32 B per entry per lane, capacity = the peak (>= 4)
+        // shared-memory ready set: 24 B per entry per lane, capacity = the peak (>= 4),
+        // row tile nibble-packed
         const int cap_s = ready_cap_req > 0 ? rcap : std::min(I->ready_bound, std::max(4, want));
-        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS,
-                                                            std::max(0LL, avail / (base_lane + 32LL * cap_s)) / 32 * 32));
+        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * cap_s;
+        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / lane_s) / 32 * 32));
         // register ready set: the smallest template >= the peak
         const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
         const int Tr = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / base_lane) / 32 * 32));
@@ -504,8 +507,8 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
             I->tpp_kind = 2;
             I->tpp_rc = cap_s;
             I->tpp_threads = Ts;
-            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * Ts + 15) & ~15LL) +
-                                           (8LL * (3 * K + 2) + 32LL * cap_s) * Ts);
+            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
+                                           (8LL * (3 * K + 2) + 24LL * cap_s) * Ts);
         }
         I->tpp_ctas = std::min(I->sms, I->main.ctas);
     }
@@ -516,11 +519,11 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
 // (local search runs at the group kernel's capacity); threads = 0 if it does not fit
 void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
     const long long avail = static_cast<long long>(MP_SMEM_DYN_MAX) - I->to.bytes - 32;
-    const long long per_lane = I->n_ops + 8LL * (3 * I->K + 2) + 32LL * cap;
+    const long long row = (I->n_ops + 1) / 2;  // nibble-packed row tile
+    const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * cap;
     const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
     *threads = T >= 64 ? T : 0;
-    *smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(I->n_ops) * T + 15) & ~15LL) + per_lane * T -
-                             static_cast<long long>(I->n_ops) * T);
+    *smem = static_cast<int>(I->to.bytes + ((row * T + 15) & ~15LL) + (per_lane - row) * T);
 }
 
 // Local search rejects a proposal whose ready set exceeds ls_cap in every kernel,
