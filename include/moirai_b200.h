@@ -128,11 +128,11 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
  * (MP_TUNE_NO_COLO) dispatches co-located flows as ordinary steps.  Results
  * never depend on these knobs. */
 #define MP_TUNE_NO_COLO 1
-#define MP_TUNE_TPP_SMEM 4  /* thread-per-placement with the ready set in shared memory even
-                               when it fits the register templates */
+#define MP_TUNE_TPP_REG 4   /* thread-per-placement with the ready set in registers (when the
+                               calibrated peak fits a 4/8/16 template) instead of shared memory */
 #define MP_TUNE_OFFCHIP 8   /* group kernel with per-placement state in global memory */
-#define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernel (it is used only
-                               with automatic G/U and a calibrated ready set <= 16) */
+#define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernels (used only with
+                               automatic G/U) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,
                          int32_t ready_cap, uint32_t flags);
 

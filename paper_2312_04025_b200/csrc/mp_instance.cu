@@ -345,8 +345,8 @@ struct mp_instance {
     DevBuf main_state, wide_state;
     // thread-per-placement variant (mp_tpp_kernel); tpp_rc == 0: not used
     bool tpp_allowed = true;
-    bool tpp_smem_pref = false;
-    bool force_offchip = false;  // MP_TUNE_OFFCHIP  // MP_TUNE_TPP_SMEM: shared-memory ready set even when registers fit
+    bool tpp_reg_pref = false;   // MP_TUNE_TPP_REG
+    bool force_offchip = false;  // MP_TUNE_OFFCHIP
     int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
     DevBuf tpp_state;
@@ -493,22 +493,22 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         // register ready set: the smallest template >= the peak
         const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
         const int Tr = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / base_lane) / 32 * 32));
-        // registers first (measured faster when the peak fits a template: C2 40.9 vs
-        // 31.4 M/s), the shared-memory ready set for wider peaks (C1: 12.4 vs 8.2 M/s
-        // for the group kernel)
-        const bool prefer_smem = I->tpp_smem_pref;
-        if (rc > 0 && Tr >= 128 && !prefer_smem) {
-            I->tpp_kind = 1;
-            I->tpp_rc = rc;
-            I->tpp_threads = Tr;
-            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * Tr + 15) & ~15LL) +
-                                           8LL * (3 * K + 2) * Tr);
-        } else if (Ts >= 128) {
+        // the shared-memory ready set first: with nibble rows and 24-byte entries it
+        // keeps as many (or more) lanes per SM and measured 1.6-1.9 % faster than
+        // the register variant on C2 / C2-K8 / C4 (46.7 vs 46.0 M/s on C2), and it is
+        // the only variant for peaks beyond 16 (C1: 22.3 M/s)
+        if (Ts >= 128 && !I->tpp_reg_pref) {
             I->tpp_kind = 2;
             I->tpp_rc = cap_s;
             I->tpp_threads = Ts;
             I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
                                            (8LL * (3 * K + 2) + 24LL * cap_s) * Ts);
+        } else if (rc > 0 && Tr >= 128) {
+            I->tpp_kind = 1;
+            I->tpp_rc = rc;
+            I->tpp_threads = Tr;
+            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>(n_ops) * Tr + 15) & ~15LL) +
+                                           8LL * (3 * K + 2) * Tr);
         }
         I->tpp_ctas = std::min(I->sms, I->main.ctas);
     }
@@ -924,7 +924,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->rcap_target = ready_cap > 0 ? ready_cap : (I->peak_probe > 0 ? std::max(4, 2 * I->peak_probe) : 32);
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
-    I->tpp_smem_pref = (flags & MP_TUNE_TPP_SMEM) != 0;
+    I->tpp_reg_pref = (flags & MP_TUNE_TPP_REG) != 0;
     I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
