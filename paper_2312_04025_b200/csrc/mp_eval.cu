@@ -483,7 +483,10 @@ __device__ __forceinline__ int group_of_lane(const EvalArgs &a, int lane, bool &
 
 // ---- K3/K4: batch evaluation with fused keep-best ---------------------------------
 template <int G, int SRC, int MODE, bool TRACE, bool COLO>
-__global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_eval_kernel(const __grid_constant__ EvalArgs a) {
+// Off-chip variants (MODE 0, state in L2) are latency-bound: 256-thread CTAs capped at
+// 64 registers so four fit per SM (32 warps in flight instead of 16).
+__global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 0 ? 4 : 1)
+    mp_eval_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ double s_best_ms[MP_CTA_MAX_THREADS / 32];
