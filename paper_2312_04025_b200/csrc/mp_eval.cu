@@ -581,7 +581,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 // an exact evaluation.  Results are identical for any G or GPU count at a fixed
 // ready capacity.
 template <int G, int MODE, bool COLO>
-__global__ void __launch_bounds__(MP_CTA_MAX_THREADS, 1) mp_ls_kernel(const __grid_constant__ EvalArgs a,
+__global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 0 ? 4 : 1) mp_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                      const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
