@@ -567,6 +567,7 @@ struct CoarsenCtx {
     unsigned char *pin = nullptr;
     size_t pin_cap = 0;
     bool smem_attr = false;
+    bool dfs_attr = false;
 };
 CoarsenCtx g_ctx[64];
 
@@ -738,6 +739,13 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
         }
         k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap);
     } else {
+        // one thread walks an L2-resident state: give the SM's unified L1 its whole
+        // capacity (no shared memory is used)
+        if (!cx.dfs_attr) {
+            CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs),
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            cx.dfs_attr = true;
+        }
         k_dfs<<<1, 32, 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf);
     }
     ++g_mp_launches;
