@@ -1238,56 +1238,26 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
         }
         // the winner's duration (not stored): op cost, payload / bw for a crossing
         // flow, 0 for a co-located flow dispatched as a node (colo off)
-        double bd = 0.0;
-        {
-            const int wn = static_cast<int>(bm & MP_NODE_MASK);
-            const uint32_t w1 = (bm >> 20) & 63u, w2 = bm >> 26;
-            if (!done && wn < n_ops) {
-                bd = T_cost[wn * K + static_cast<int>(w1)];
-            } else if (!done && w1 != RZ) {
-                const int ka = static_cast<int>(w1) - K, kb = static_cast<int>(w2) - 2 * K;
-                bd = div_bw(T_fpay[wn - n_ops], T_bw[ka * K + kb], T_rbw[ka * K + kb], fast);
-            }
-        }
-        // unordered removal: the last entry moves into the hole
-        const int last = nr - 1;
-        if (!done && bs != last) {
-            const int o = bs * T + tid, ol = last * T + tid;
-            rE[o] = rE[ol];
-            rR[o] = rR[ol];
-            rM[o] = rM[ol];
-        }
-        nr = done ? nr : last;
-        // -- commit (solver.py:130-138) ------------------------------------------------
-        const double end = bitsd(be) + bd;
+        // The winner is known: issue the successors' global loads (first group of SU)
+        // before the duration, the removal and the commit, so their latency overlaps
+        // that work.  Phase A reads only the row tile, the tables and the global
+        // rank / multi-input state, none of which the removal or the commit writes.
         const int node = static_cast<int>(bm & MP_NODE_MASK);
         const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
-        if (!done) {
-            clk[(r1 == RZ ? WS : r1) * T + tid] = end;
-            clk[(r2 == RZ ? WS : r2) * T + tid] = end;
-        }
         const bool isop = node < n_ops;
-        ms = (!done && isop && end > ms) ? end : ms;
-        // -- successors (solver.py:140-145), one uniform loop over the warp's
-        //    largest successor count: op -> its out-flows, flow -> its consumer ---------
         const int d = static_cast<int>(r1);
         const int nodec = done ? 0 : node;
         const int ob = static_cast<int>(T_out_beg[isop ? nodec : 0]);
         const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
         const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
         const int maxc = __reduce_max_sync(kFull, cnt);
-        // Successors are processed SU at a time: every global load of the group
-        // (rank of the consumer, multi-input state) is issued before any of them is
-        // used, so their latencies overlap.  The consumers of one step are distinct
-        // (no parallel edges), so the hoisted loads never read a value written
-        // earlier in the same group.
         constexpr int SU = 2;
-        for (int t0 = 0; t0 < maxc; t0 += SU) {
-            int j_[SU], dj_[SU];
-            uint32_t pid_[SU], np1_[SU], ct_[SU];
-            long long mo_[SU];
-            double rj_[SU], cur_[SU], pay_[SU];
-            bool act_[SU], multi_[SU];
+        int j_[SU], dj_[SU];
+        uint32_t pid_[SU], np1_[SU], ct_[SU];
+        long long mo_[SU];
+        double rj_[SU], cur_[SU], pay_[SU];
+        bool act_[SU], multi_[SU];
+        auto phase_a = [&](int t0) {
 #pragma unroll
             for (int u = 0; u < SU; ++u) {
                 const int t = t0 + u;
@@ -1315,6 +1285,39 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
                     ct_[u] = g_mtie[mo_[u]];
                 }
             }
+        };
+        if (maxc > 0) phase_a(0);
+        // the winner's duration (not stored): op cost, payload / bw for a crossing
+        // flow, 0 for a co-located flow dispatched as a node (colo off)
+        double bd = 0.0;
+        if (!done && isop) {
+            bd = T_cost[node * K + d];
+        } else if (!done && r1 != RZ) {
+            const int ka = d - K, kb = static_cast<int>(r2) - 2 * K;
+            bd = div_bw(T_fpay[node - n_ops], T_bw[ka * K + kb], T_rbw[ka * K + kb], fast);
+        }
+        // unordered removal: the last entry moves into the hole
+        const int last = nr - 1;
+        if (!done && bs != last) {
+            const int o = bs * T + tid, ol = last * T + tid;
+            rE[o] = rE[ol];
+            rR[o] = rR[ol];
+            rM[o] = rM[ol];
+        }
+        nr = done ? nr : last;
+        // -- commit (solver.py:130-138) ------------------------------------------------
+        const double end = bitsd(be) + bd;
+        if (!done) {
+            clk[(r1 == RZ ? WS : r1) * T + tid] = end;
+            clk[(r2 == RZ ? WS : r2) * T + tid] = end;
+        }
+        ms = (!done && isop && end > ms) ? end : ms;
+        // -- successors (solver.py:140-145), one uniform loop over the warp's largest
+        //    successor count: op -> its out-flows, flow -> its consumer.  The consumers
+        //    of one step are distinct (no parallel edges), so loads hoisted for a group
+        //    never read a value written earlier in the same step. -------------------------
+        for (int t0 = 0; t0 < maxc; t0 += SU) {
+            if (t0 > 0) phase_a(t0);
 #pragma unroll
             for (int u = 0; u < SU; ++u) {
                 if (t0 + u >= maxc) break;
