@@ -469,7 +469,9 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         m.U = 32;
         m.threads = 256;
         m.groups_per_cta = (m.threads / 32) * (32 / m.G);
-        const int per_sm = ctas_per_sm_req > 0 ? ctas_per_sm_req : 4;  // 64-register CTAs: four per SM
+        // 64-register CTAs: four per SM; two for 32-lane groups (ready sets of thousands,
+        // where the per-placement latency, not the number in flight, dominates)
+        const int per_sm = ctas_per_sm_req > 0 ? ctas_per_sm_req : (m.G >= 32 ? 2 : 4);
         long long g2 = static_cast<long long>(I->sms) * per_sm * m.groups_per_cta;
         while (g2 > m.groups_per_cta && g2 * static_cast<long long>(so.bytes) > budget) g2 /= 2;
         m.ctas = static_cast<int>(std::max(1LL, g2 / m.groups_per_cta));
