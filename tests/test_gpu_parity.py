@@ -136,7 +136,7 @@ def test_gcof_rejects_cycles_and_is_idempotent():
 def test_gcof_large_synthetic_vs_oracle(oracle_mod):
     from paper_2312_04025_b200.fusion import _Flat
 
-    for n, seed in ((5000, 1), (20000, 2)):
+    for n, seed in ((5000, 1), (20000, 2), (100_000, 3)):  # up to the C5 sweep's largest graph
         g = mp.gen_synthetic(mp.GenSpec(ops=n, width=32, density=0.5, devices=(0, 1, 2, 3)), seed)
         rules = workloads.table_rules()
         out = mp.gcof(g, rules)
@@ -412,3 +412,36 @@ def test_large_graph_and_batch_vs_oracle(oracle_mod):
         assert np.array_equal(bits(ms[idx]), bits(want))
         best, bms = mp.argmin(inst, big)
         assert bms == ms.min() and best == int(np.argmin(ms))
+
+
+def test_concurrent_callers_share_an_instance(oracle_mod):
+    """Instances are immutable after creation; concurrent callers on several host
+    threads (each call serialised on the instance's stream) get exact results."""
+    import threading
+
+    w = workloads.c2(4)
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        orc = oracle_mod.OracleInstance.from_instance(inst)
+        batches = [workloads.placements(100 + t, 3000, inst.n_ops, inst.K) for t in range(6)]
+        results = [None] * 6
+        errors = []
+
+        def work(t):
+            try:
+                results[t] = (mp.evaluate_batch(inst, batches[t]), mp.argmin(inst, batches[t]),
+                              mp.local_search(inst, batches[t][:4], chains=64, moves=8, seed=t)[1])
+            except Exception as e:  # pragma: no cover - surfaced below
+                errors.append(e)
+
+        threads = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        assert not errors, errors
+        for t in range(6):
+            want, _ = orc.eval_batch(batches[t], threads=8)
+            ms, (best, bms), _ = results[t]
+            assert np.array_equal(bits(ms), bits(want))
+            assert best == int(np.argmin(want)) and bms == want.min()
