@@ -362,6 +362,7 @@ struct mp_instance {
     DevBuf rows_dev[2];
     DevBuf out_dev[2];
     DevBuf small;     // argmin result / enum tables / trace
+    DevBuf ls_buf;    // local-search seeds, chain rows and makespans
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     cudaEvent_t ev_copy[2]{}, ev_used[2]{};
     std::mutex mu;
@@ -1418,7 +1419,7 @@ extern "C" int32_t mp_local_search(mp_instance *I, const uint8_t *seed_rows, int
     }
     const size_t seed_b = align16(static_cast<size_t>(n_seed) * n);
     const size_t rows_b = align16(static_cast<size_t>(n_chains) * n);
-    DevBuf buf;
+    DevBuf &buf = I->ls_buf;  // kept across calls (grows only)
     MP_CUDA(buf.ensure(seed_b + rows_b + 8ULL * n_chains + 64));
     unsigned char *base = static_cast<unsigned char *>(buf.p);
     uint8_t *dseed = base;
