@@ -51,11 +51,22 @@ def combine_records(records) -> tuple[float, int]:
     return float(np.int64(best[0]).view(np.float64)), best[1]
 
 
+def _single(group) -> bool:
+    """No process group formed: a single rank (the exchange is the identity)."""
+    import torch.distributed as dist
+
+    return not (dist.is_available() and dist.is_initialized())
+
+
 def allgather_best(best_ms: float, best_row: int, group=None, device=None) -> tuple[float, int]:
     """All-gather every rank's local best (16 B each) and return the global best.
-    Uses the default process group's backend (NCCL on GPUs, gloo on CPU)."""
+    Uses the default process group's backend (NCCL on GPUs, gloo on CPU); without
+    a process group it is the identity (one rank)."""
     import torch
     import torch.distributed as dist
+
+    if _single(group):
+        return combine_records(encode_record(best_ms, best_row))
 
     rec = torch.from_numpy(encode_record(best_ms, best_row))
     if device is not None:
@@ -88,6 +99,9 @@ def broadcast_row(row: np.ndarray, src: int, group=None, device=None) -> np.ndar
     import torch
     import torch.distributed as dist
 
+    if _single(group):
+        return np.ascontiguousarray(row, dtype=np.uint8).copy()
+
     t = torch.from_numpy(np.ascontiguousarray(row, dtype=np.uint8).copy())
     if device is not None:
         t = t.to(device)
@@ -103,7 +117,8 @@ def distributed_local_search(inst, seeds: np.ndarray, *, rounds: int, chains: in
     the ranks all-gather a 16-byte ``(makespan bits, global chain)`` record, the
     owner of the lexicographic minimum broadcasts its row, and the next round
     starts every chain from that incumbent.  Results are independent of the world
-    size.  ``search(inst, seeds, chains, chain_base, moves, rng_seed) -> (row, ms,
+    size; with ``world=1`` and no process group it is a single-GPU multi-round
+    incumbent-improvement loop.  ``search(inst, seeds, chains, chain_base, moves, rng_seed) -> (row, ms,
     chain)`` defaults to the GPU :func:`paper_2312_04025_b200.local_search`; the
     CPU tests inject the oracle's restatement.  Returns ``(row, makespan)``."""
     if search is None:

@@ -153,3 +153,28 @@ def test_distributed_local_search_is_world_size_independent(world, oracle_mod):
         p.join(timeout=60)
     assert all(v[1] == best for v in got.values()), (got, best)
     assert all(v == got[0] for v in got.values())
+
+
+def test_local_search_rounds_without_a_process_group(oracle_mod):
+    """world=1 without torch.distributed: the same rounds as the reference loop."""
+    from oracle.oracle import OracleInstance, ls_chains
+    from paper_2312_04025_b200.distributed import distributed_local_search
+
+    arrays = _ls_instance()
+    seeds = np.random.default_rng(2).integers(0, 3, (4, 10), dtype=np.uint8)
+    orc = OracleInstance(*arrays)
+
+    def search(_inst, s, n, base, moves, rs):
+        row, ms, ch, _ = ls_chains(orc, s, n, base, moves, rs)
+        return row, ms, ch
+
+    row, ms = distributed_local_search(None, seeds, rounds=3, chains=24, moves=6, seed=5, rank=0, world=1,
+                                       search=search)
+    cur, best = seeds, math.inf
+    for r in range(3):
+        w_row, w_ms, _, _ = ls_chains(orc, cur, 24, 0, 6, 5 + r)
+        best = min(best, w_ms)
+        cur = w_row.reshape(1, -1)
+    assert ms == best
+    st, rms, *_ = orc.schedule(row)
+    assert st == 0 and rms == ms
