@@ -1251,7 +1251,10 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
         const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
         const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
         const int maxc = __reduce_max_sync(kFull, cnt);
-        constexpr int SU = 2;
+#ifndef MP_TPPS_SU
+#define MP_TPPS_SU 2
+#endif
+        constexpr int SU = MP_TPPS_SU;
         int j_[SU], dj_[SU];
         uint32_t pid_[SU], np1_[SU], ct_[SU];
         long long mo_[SU];
