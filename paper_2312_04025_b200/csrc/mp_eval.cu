@@ -135,7 +135,7 @@ __device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &
 // of a group returns the group's result.
 template <int G, bool TRACE, bool COLO>
 __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsigned char *tb, unsigned char *st,
-                                                   unsigned char *dev, int gl, bool live) {
+                                                   unsigned char *dev, int gl, bool live, double *clk_) {
     const int lane = threadIdx.x & 31;
     const unsigned gbits = group_bits<G>(lane);
     const unsigned below = gbits & ((1u << lane) - 1u);
@@ -152,7 +152,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     res.peak = 0;
 
     // ---- 1. memory feasibility (solver.py:82-87) ------------------------------
-    double *clk = slot<double>(st, a.so.clk);
+    double *clk = clk_;  // the group's resource clocks (shared memory in every mode)
     unsigned long long *load = reinterpret_cast<unsigned long long *>(clk);
     for (int k = gl; k < K; k += G) load[k] = 0ULL;
     __syncwarp();
@@ -499,6 +499,10 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
     const unsigned char *tb;
     unsigned char *st;
     group_bases<MODE>(sm, a, grp, &s_bar, tb, st);
+    // off-chip state keeps its 3K+2 resource clocks in shared memory all the same
+    // (read for every scanned ready entry)
+    double *clkp = MODE == 0 ? reinterpret_cast<double *>(sm) + static_cast<size_t>(grp) * (3 * a.K + 2)
+                             : slot<double>(st, a.so.clk);
     unsigned char *devbuf = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) devbuf[i] = 0;
     double best_ms = kInf;
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             dev = devbuf;
         }
         __syncwarp();
-        const RowResult r = eval_lockstep<G, TRACE, COLO>(a, tb, st, dev, gl, live);
+        const RowResult r = eval_lockstep<G, TRACE, COLO>(a, tb, st, dev, gl, live, clkp);
         if (live && gl == 0 && a.peak_ready) atomicMax(a.peak_ready, static_cast<unsigned int>(r.peak));
         if (live && gl == 0) {
             const long long o = grow - a.out_base;
@@ -593,6 +597,10 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
     const unsigned char *tb;
     unsigned char *st;
     group_bases<MODE>(sm, a, grp, &s_bar, tb, st);
+    // off-chip state keeps its 3K+2 resource clocks in shared memory all the same
+    // (read for every scanned ready entry)
+    double *clkp = MODE == 0 ? reinterpret_cast<double *>(sm) + static_cast<size_t>(grp) * (3 * a.K + 2)
+                             : slot<double>(st, a.so.clk);
     unsigned char *dev = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) dev[i] = 0;
     const int n = a.n_ops, K = a.K;
@@ -609,7 +617,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             for (int i = gl; i < n; i += G) dev[i] = seed[i];
         }
         __syncwarp();
-        RowResult cur = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live);
+        RowResult cur = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live, clkp);
         double cur_ms = cur.status == MP_ROW_OK ? cur.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
@@ -619,7 +627,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             __syncwarp();
             if (live && gl == 0) dev[i] = static_cast<unsigned char>(nd);
             __syncwarp();
-            const RowResult r = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live);
+            const RowResult r = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live, clkp);
             const double ms = r.status == MP_ROW_OK ? r.ms : kInf;
             __syncwarp();
             if (r.status != MP_ROW_OVERFLOW && ms <= cur_ms) {
@@ -1708,7 +1716,8 @@ cudaError_t mp_eval_set_smem_limits() {
 cudaError_t mp_launch_eval(const LaunchShape &ls, int src_mode, bool trace, const EvalArgs &a, cudaStream_t s) {
     const int mode = trace ? 0 : ls.mode;
     EvalFn f = pick_any(ls.G, src_mode, mode, trace, a.colo != 0);
-    f<<<ls.ctas, ls.threads, mode ? ls.smem : 0, s>>>(a);
+    const int smem0 = (a.groups_per_cta + 1) * (3 * a.K + 2) * 8;  // mode 0: the clocks only
+    f<<<ls.ctas, ls.threads, mode ? ls.smem : smem0, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
 }
@@ -1796,7 +1805,8 @@ cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a
 
 cudaError_t mp_launch_ls(const LaunchShape &shape, const EvalArgs &a, const LsArgs &ls, cudaStream_t s) {
     LsFn f = pick_ls(shape.G, shape.mode, a.colo != 0);
-    f<<<shape.ctas, shape.threads, shape.mode ? shape.smem : 0, s>>>(a, ls);
+    const int smem0 = (a.groups_per_cta + 1) * (3 * a.K + 2) * 8;
+    f<<<shape.ctas, shape.threads, shape.mode ? shape.smem : smem0, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();
 }

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out; rm -f gpurun_out/c5c.txt
+for spec in "c5:1000:4 65536" "c5:2000:4 32768" "c5:5000:8 16384" "c5:10000:8 16384"; do
+  set -- $spec
+  timeout 400 python scripts/prof_eval.py --workload $1 --rows $2 --iters 3 >> gpurun_out/c5c.txt 2>&1
+done
+timeout 300 python scripts/prof_eval.py --workload c3 --rows 1048576 --iters 3 >> gpurun_out/c5c.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bnb.py -x -q > gpurun_out/pytest_c5.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_c5.log
