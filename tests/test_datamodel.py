@@ -181,3 +181,33 @@ def test_public_surface_names():
                  "fused_cost", "gcof", "gen_synthetic", "match_rule", "schedule_for_assignment", "simulate",
                  "solve_exact", "topo_order", "validate_dag"):
         assert hasattr(mp, name), name
+
+
+def test_mip_start_names_and_values_follow_the_reference_model():
+    """x/z/u/S/C values of a schedule in the reference MILP's naming (milp.py:151-160);
+    reading them back gives the same assignment, channels and times."""
+    from paper_2312_04025_b200.mipstart import mip_start_text
+
+    c = mp.Cluster([mp.Device(0, 100), mp.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
+    g = mp.CompGraph([mp.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}), mp.OpNode(2, "bn", 10, {0: 1.0, 1: 0.5})],
+                     [mp.FlowEdge(1, 2, 10_000_000)])
+    s = mp.Schedule({1: 0, 2: 1}, {1: 0.0, 3: 2.0, 2: 4.0}, {1: 2.0, 3: 4.0, 2: 4.5}, {3: (0, 1)}, 4.5)
+    text = mip_start_text(s, g, c)
+    vals = {ln.split()[0]: float(ln.split()[1]) for ln in text.splitlines() if not ln.startswith("#")}
+    assert {k for k, v in vals.items() if k.startswith("x_") and v == 1.0} == {"x_1_0", "x_2_1"}
+    assert vals["z_3"] == 1.0 and vals["u_3_0_1"] == 1.0 and vals["u_3_1_0"] == 0.0
+    assert (vals["S_2"], vals["C_2"], vals["S_3"], vals["C_3"]) == (4.0, 4.5, 2.0, 4.0)
+    import sys
+    from pathlib import Path
+
+    ref = Path("/root/reference/pkg/src")
+    if ref.exists():  # the reference's own model declares exactly these names (here only)
+        sys.path.insert(0, str(ref))
+        import opplace
+
+        rc = opplace.Cluster([opplace.Device(0, 100), opplace.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
+        rg = opplace.CompGraph([opplace.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}),
+                                opplace.OpNode(2, "bn", 10, {0: 1.0, 1: 0.5})], [opplace.FlowEdge(1, 2, 10_000_000)])
+        mdl = opplace.build_model(rg, rc, opplace.effective_bandwidth(rc))
+        names = {v.name for v in mdl.vars}
+        assert set(vals) <= names
