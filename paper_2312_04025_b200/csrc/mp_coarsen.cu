@@ -191,10 +191,10 @@ __global__ void __launch_bounds__(1024) k_kahn(int V, const int *obeg, const int
     if (threadIdx.x == 0) *seen = total;
 }
 
-// Distinct current groups of the input successors of `t`, excluding `self`.
-// Returns the count, stopping early at 2 when `cap` == 2.
+// Distinct current groups of the input successors of `t`, excluding `self`
+// (scalar form, any out-degree): written to buf[0..n), returns n.
 __device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, const int *odst, int t, int self,
-                                          int *buf, int cap) {
+                                          int *buf) {
     int n = 0;
     for (int q = obeg[t]; q < obeg[t + 1]; ++q) {
         const int w = s.where[odst[q]];
@@ -206,28 +206,73 @@ __device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, co
                 break;
             }
         if (dup) continue;
-        if (n == cap) return n + 1;
         buf[n++] = w;
     }
     return n;
 }
 
-// The reference DFS (fusion.py:281-303), replayed exactly by one thread over
-// the state `s` (shared or global memory, see k_dfs_smem).
+// The same set gathered by a whole warp when out-degree <= 32: lane k loads
+// successor k's group (one dependent chain instead of one per successor); the
+// first lane holding each distinct group is its "leader".
+struct OutSet {
+    int n;          // distinct groups (warp-uniform)
+    int one;        // the group when n == 1
+    int w;          // this lane's group, -1 if none / self
+    bool lead;      // this lane represents w
+    bool wide;      // out-degree > 32: the set is in buf[0..n) (scalar form)
+};
+
+__device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *obeg, const int *odst, int t, int self,
+                                                  int *buf) {
+    const int lane = threadIdx.x & 31;
+    const int b = obeg[t], e = obeg[t + 1];
+    OutSet o;
+    o.wide = e - b > 32;
+    if (o.wide) {
+        o.n = out_groups(s, obeg, odst, t, self, buf);
+        o.one = buf[0];
+        o.w = -1;
+        o.lead = false;
+        return o;
+    }
+    int w = -1;
+    if (b + lane < e) {
+        const int x = s.where[odst[b + lane]];
+        w = x == self ? -1 : x;
+    }
+    const unsigned same = __match_any_sync(0xffffffffu, w);
+    o.lead = w >= 0 && (same & ((1u << lane) - 1u)) == 0u;
+    const unsigned L = __ballot_sync(0xffffffffu, o.lead);
+    o.n = __popc(L);
+    o.one = __shfl_sync(0xffffffffu, w, L ? __ffs(L) - 1 : 0);
+    o.w = w;
+    return o;
+}
+
+// The reference DFS (fusion.py:281-303), replayed exactly by one warp over the
+// state `s` (shared or global memory, see k_dfs_smem).  Every lane runs the
+// same scalar replay (same loads, same stores of the same values, so each lane
+// reads back its own writes); the warp splits only the successor gathers, the
+// visited tests of the successors and the source scan.
 __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, const Trie &t,
                         const DfsState &s, int *stack, int *buf) {
-    int two[2];
-    for (int src = 0; src < V; ++src) {
-        if (indeg[src] != 0) continue;  // sources of the input graph, ascending id
+    const int lane = threadIdx.x & 31;
+    for (int s0 = 0; s0 < V; s0 += 32) {
+        // sources of the input graph, ascending id
+        unsigned srcs = __ballot_sync(0xffffffffu, s0 + lane < V && indeg[s0 + lane] == 0);
+        for (; srcs; srcs &= srcs - 1u) {
+        const int src = s0 + __ffs(srcs) - 1;
         int sp = 0;
         stack[sp++] = src;
         while (sp > 0) {
             int cur = s.where[stack[--sp]];
             if (s.visited[cur]) continue;
+            OutSet os;
             for (;;) {
                 // |out[cur]| == 1 ?  (fusion.py:291-294)
-                if (out_groups(s, obeg, odst, s.tail[cur], cur, two, 1) != 1) break;
-                const int nxt = two[0];
+                os = out_groups_warp(s, obeg, odst, s.tail[cur], cur, buf);
+                if (os.n != 1) break;
+                const int nxt = os.one;
                 // _match_seqs(seqs[cur], seqs[nxt]) (fusion.py:93-104) via the trie
                 const int ln = s.len[nxt];
                 int st = s.state[cur];
@@ -270,8 +315,19 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
             }
             s.visited[cur] = 1;
             // push unvisited out groups in descending id (fusion.py:301-303)
-            const int no = out_groups(s, obeg, odst, s.tail[cur], cur, buf, 0x7fffffff);
-            // insertion sort ascending (out-degrees are small; worst case is still exact)
+            if (!os.wide) {
+                // position of a pushed group = number of pushed groups above it
+                const bool push = os.lead && !s.visited[os.w];
+                const unsigned P = __ballot_sync(0xffffffffu, push);
+                int above = 0;
+                for (unsigned m = P; m; m &= m - 1u) above += __shfl_sync(0xffffffffu, os.w, __ffs(m) - 1) > os.w;
+                if (push) stack[sp + above] = os.w;
+                sp += __popc(P);
+                __syncwarp();
+                continue;
+            }
+            const int no = os.n;
+            // insertion sort ascending (worst case is still exact)
             for (int i = 1; i < no; ++i) {
                 const int v = buf[i];
                 int j = i - 1;
@@ -284,17 +340,18 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
             for (int z = no - 1; z >= 0; --z)
                 if (!s.visited[buf[z]]) stack[sp++] = buf[z];
         }
+        }
     }
 }
 
 __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
                       int *stack, int *buf) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (threadIdx.x >= 32 || blockIdx.x != 0) return;
     dfs_run(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
 }
 
 // Small graphs: the whole DFS state, CSR and trie move into shared memory (one
-// CTA), the DFS runs on thread 0 at shared-memory latency, and the state is
+// CTA), the DFS runs on warp 0 at shared-memory latency, and the state is
 // written back for the parallel final partition.
 __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int TN, const int *indeg, const int *obeg,
                                                    const int *odst, Trie tg, DfsState sg, int stack_cap) {
@@ -346,7 +403,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
         t.flags[i] = tg.flags[i];
     }
     __syncthreads();
-    if (threadIdx.x == 0) dfs_run(V, Lmax, ind, ob, od, t, s, stack, buf);
+    if (threadIdx.x < 32) dfs_run(V, Lmax, ind, ob, od, t, s, stack, buf);  // warp 0
     __syncthreads();
     for (int i = threadIdx.x; i < V; i += blockDim.x) {
         sg.where[i] = s.where[i];

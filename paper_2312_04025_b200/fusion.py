@@ -148,7 +148,8 @@ class _Flat:
         dindex = {d: i for i, d in enumerate(self.devices)}
         D = len(self.devices)
         if uniform and V and list(first) == self.devices:
-            cost = np.array([list(ct.values()) for ct in cts], dtype=np.float64).reshape(V, max(D, 1))
+            cost = np.fromiter(chain.from_iterable(map(dict.values, cts)), dtype=np.float64,
+                               count=V * D).reshape(V, max(D, 1))
         else:
             cost = np.full((V, max(D, 1)), np.nan)
             for i, ct in enumerate(cts):
