@@ -120,14 +120,16 @@ struct DfsState {
     int *len;       // [V] by group id: sequence length (capped at Lmax+1)
     int *seq;       // [V*Lmax] by group id: the sequence (valid when len <= Lmax)
     int *tag;       // [V] by group id
+    int2 *obt;      // [V] by group id: out-edge range [obeg[tail], obeg[tail+1]) of the group's tail
     unsigned char *visited;  // [V] by group id
 };
 
 // Initial per-node state: singleton groups with the node's own type sequence.
 __global__ void k_init_nodes(int V, int Lmax, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
-                             DfsState s) {
+                             const int *obeg, DfsState s) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         s.where[v] = v;
+        s.obt[v] = make_int2(obeg[v], obeg[v + 1]);
         s.next[v] = -1;
         s.head[v] = v;
         s.tail[v] = v;
@@ -193,10 +195,9 @@ __global__ void __launch_bounds__(1024) k_kahn(int V, const int *obeg, const int
 
 // Distinct current groups of the input successors of `t`, excluding `self`
 // (scalar form, any out-degree): written to buf[0..n), returns n.
-__device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, const int *odst, int t, int self,
-                                          int *buf) {
+__device__ __forceinline__ int out_groups(const DfsState &s, const int *odst, int2 ob, int self, int *buf) {
     int n = 0;
-    for (int q = obeg[t]; q < obeg[t + 1]; ++q) {
+    for (int q = ob.x; q < ob.y; ++q) {
         const int w = s.where[odst[q]];
         if (w == self) continue;
         bool dup = false;
@@ -212,48 +213,59 @@ __device__ __forceinline__ int out_groups(const DfsState &s, const int *obeg, co
 }
 
 // The same set gathered by a whole warp when out-degree <= 32: lane k loads
-// successor k's group (one dependent chain instead of one per successor); the
-// first lane holding each distinct group is its "leader".
+// successor k's group, and with it that group's visited flag and sequence
+// length (one dependent chain instead of one per successor); the first lane
+// holding each distinct group is its "leader".
 struct OutSet {
     int n;          // distinct groups (warp-uniform)
     int one;        // the group when n == 1
+    int one_len;    // its sequence length (valid when n == 1)
     int w;          // this lane's group, -1 if none / self
     bool lead;      // this lane represents w
+    bool vis;       // visited[w] (leaders)
     bool wide;      // out-degree > 32: the set is in buf[0..n) (scalar form)
 };
 
-__device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *obeg, const int *odst, int t, int self,
-                                                  int *buf) {
+__device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *odst, int2 ob, int self, int *buf) {
     const int lane = threadIdx.x & 31;
-    const int b = obeg[t], e = obeg[t + 1];
     OutSet o;
-    o.wide = e - b > 32;
+    o.wide = ob.y - ob.x > 32;
     if (o.wide) {
-        o.n = out_groups(s, obeg, odst, t, self, buf);
+        o.n = out_groups(s, odst, ob, self, buf);
         o.one = buf[0];
+        o.one_len = o.n == 1 ? s.len[o.one] : 0;
         o.w = -1;
-        o.lead = false;
+        o.lead = o.vis = false;
         return o;
     }
-    int w = -1;
-    if (b + lane < e) {
-        const int x = s.where[odst[b + lane]];
+    int w = -1, lw = 0;
+    bool vis = true;
+    if (ob.x + lane < ob.y) {
+        const int x = s.where[odst[ob.x + lane]];
+        vis = s.visited[x];  // x is a live group id even when it is `self`
+        lw = s.len[x];
         w = x == self ? -1 : x;
     }
     const unsigned same = __match_any_sync(0xffffffffu, w);
     o.lead = w >= 0 && (same & ((1u << lane) - 1u)) == 0u;
     const unsigned L = __ballot_sync(0xffffffffu, o.lead);
     o.n = __popc(L);
-    o.one = __shfl_sync(0xffffffffu, w, L ? __ffs(L) - 1 : 0);
+    const int src = L ? __ffs(L) - 1 : 0;
+    o.one = __shfl_sync(0xffffffffu, w, src);
+    o.one_len = __shfl_sync(0xffffffffu, lw, src);
     o.w = w;
+    o.vis = vis;
     return o;
 }
 
 // The reference DFS (fusion.py:281-303), replayed exactly by one warp over the
 // state `s` (shared or global memory, see k_dfs_smem).  Every lane runs the
 // same scalar replay (same loads, same stores of the same values, so each lane
-// reads back its own writes); the warp splits only the successor gathers, the
-// visited tests of the successors and the source scan.
+// reads back its own writes); the warp splits the successor gathers (with the
+// successors' visited flags and lengths), the rule match's sequence loads, the
+// sequence concatenation and the source scan.  Per DFS node the dependent
+// chain is stack -> where -> {visited, tail range, trie state, length} ->
+// successor -> its group -> {visited, length}.
 __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, const Trie &t,
                         const DfsState &s, int *stack, int *buf) {
     const int lane = threadIdx.x & 31;
@@ -266,18 +278,24 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
         stack[sp++] = src;
         while (sp > 0) {
             int cur = s.where[stack[--sp]];
-            if (s.visited[cur]) continue;
+            // independent loads of cur's record, issued together
+            const bool seen = s.visited[cur];
+            int2 ob = s.obt[cur];
+            int st_cur = s.state[cur];
+            int len_cur = s.len[cur];
+            if (seen) continue;
             OutSet os;
             for (;;) {
                 // |out[cur]| == 1 ?  (fusion.py:291-294)
-                os = out_groups_warp(s, obeg, odst, s.tail[cur], cur, buf);
+                os = out_groups_warp(s, odst, ob, cur, buf);
                 if (os.n != 1) break;
                 const int nxt = os.one;
                 // _match_seqs(seqs[cur], seqs[nxt]) (fusion.py:93-104) via the trie
-                const int ln = s.len[nxt];
-                int st = s.state[cur];
-                if (st < 0 || ln > Lmax || s.len[cur] + ln > Lmax) break;
-                for (int q = 0; q < ln && st >= 0; ++q) st = trie_step(t, st, s.seq[static_cast<size_t>(nxt) * Lmax + q]);
+                const int ln = os.one_len;
+                if (st_cur < 0 || ln > Lmax || len_cur + ln > Lmax) break;
+                const int sn = lane < ln ? s.seq[static_cast<size_t>(nxt) * Lmax + lane] : 0;  // nxt's types
+                int st = st_cur;
+                for (int q = 0; q < ln; ++q) st = trie_step(t, st, __shfl_sync(0xffffffffu, sn, q));
                 if (st < 0) break;
                 const int fl = t.flags[st];
                 int kind;  // 2 prefix (wins), 1 full
@@ -286,12 +304,12 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 else break;
                 // combine(cur, nxt) (fusion.py:169-190)
                 const int nw = cur < nxt ? cur : nxt;
-                const int lc = s.len[cur];
-                int tmp[32];
-                const int L2 = lc + ln;
-                for (int q = 0; q < lc; ++q) tmp[q] = s.seq[static_cast<size_t>(cur) * Lmax + q];
-                for (int q = 0; q < ln; ++q) tmp[lc + q] = s.seq[static_cast<size_t>(nxt) * Lmax + q];
+                const int lc = len_cur;
+                const int L2 = lc + ln;  // <= Lmax <= 30: lane q moves element q
+                const int from_n = __shfl_sync(0xffffffffu, sn, (lane - lc) & 31);
+                const int sv = lane < lc ? s.seq[static_cast<size_t>(cur) * Lmax + lane] : from_n;
                 const int h_cur = s.head[cur], t_cur = s.tail[cur], h_nxt = s.head[nxt], t_nxt = s.tail[nxt];
+                const int2 ob_nxt = s.obt[nxt];
                 // rename the members of the group whose id disappears
                 if (nw == cur) {
                     for (int x = h_nxt;; x = s.next[x]) {
@@ -307,17 +325,23 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.next[t_cur] = h_nxt;
                 s.head[nw] = h_cur;
                 s.tail[nw] = t_nxt;
+                s.obt[nw] = ob_nxt;
                 s.len[nw] = L2;
-                for (int q = 0; q < L2; ++q) s.seq[static_cast<size_t>(nw) * Lmax + q] = tmp[q];
+                __syncwarp();
+                if (lane < L2) s.seq[static_cast<size_t>(nw) * Lmax + lane] = sv;
+                __syncwarp();
                 s.state[nw] = st;
                 s.tag[nw] = kind == 2 ? kTagBound : kTagFused;
                 cur = nw;
+                ob = ob_nxt;
+                st_cur = st;
+                len_cur = L2;
             }
             s.visited[cur] = 1;
             // push unvisited out groups in descending id (fusion.py:301-303)
             if (!os.wide) {
                 // position of a pushed group = number of pushed groups above it
-                const bool push = os.lead && !s.visited[os.w];
+                const bool push = os.lead && !os.vis;
                 const unsigned P = __ballot_sync(0xffffffffu, push);
                 int above = 0;
                 for (unsigned m = P; m; m &= m - 1u) above += __shfl_sync(0xffffffffu, os.w, __ffs(m) - 1) > os.w;
@@ -371,6 +395,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
     s.len = take(V);
     s.tag = take(V);
     s.seq = take(V * Lmax);
+    s.obt = reinterpret_cast<int2 *>(take(2 * V));
     int *ind = take(V);
     int *ob = take(V + 1);
     int *od = take(E);
@@ -390,6 +415,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
         s.state[i] = sg.state[i];
         s.len[i] = sg.len[i];
         s.tag[i] = sg.tag[i];
+        s.obt[i] = sg.obt[i];
         s.visited[i] = 0;
         ind[i] = indeg[i];
     }
@@ -419,7 +445,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
 
 size_t dfs_smem_bytes(int V, int E, int Lmax, int TN, int stack_cap) {
     auto r4 = [](size_t n) { return (n + 3) & ~size_t(3); };
-    return 4 * (7 * r4(V) + r4(static_cast<size_t>(V) * Lmax) + r4(V) + r4(V + 1) + r4(E) + 4 * r4(TN) +
+    return 4 * (7 * r4(V) + r4(2 * static_cast<size_t>(V)) + r4(static_cast<size_t>(V) * Lmax) + r4(V) + r4(V + 1) + r4(E) + 4 * r4(TN) +
                 2 * r4(stack_cap)) + static_cast<size_t>(V) + 16;
 }
 
@@ -709,7 +735,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
                                    std::max(E, 1));
     const size_t tmpb = std::max(std::max(tmp_bytes, t2), std::max(t3, t4)) + 256;
     size_t need = up_used + tmpb + 96 * 512;
-    need += 4ULL * ((V + 1ULL) * 40 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
+    need += 4ULL * ((V + 1ULL) * 42 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
     need += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
     if (cx.dev_cap < need) {
         if (cx.dev) cudaFree(cx.dev);
@@ -779,13 +805,14 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     s.len = ar.take<int>(V);
     s.seq = ar.take<int>(static_cast<size_t>(V) * Lmax);
     s.tag = ar.take<int>(V);
+    s.obt = ar.take<int2>(V);
     s.visited = ar.take<unsigned char>(V);
     const int stack_cap = E + V + 8;
     int *stack = ar.take<int>(stack_cap), *buf = ar.take<int>(stack_cap);
     int *ntrie = ar.take<int>(4);
     k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
     ++g_mp_launches;
-    k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, s);
+    k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, obeg, s);
     ++g_mp_launches;
     const size_t dsm = dfs_smem_bytes(V, E, Lmax, TN, stack_cap);
     if (dsm <= static_cast<size_t>(MP_SMEM_DYN_MAX)) {

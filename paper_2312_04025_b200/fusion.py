@@ -234,8 +234,8 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
             gid_of.append(n.id)
             continue
         parts = [nodes_in[m] for m in mlist[mb[z]:mb[z + 1]]]
-        seq = tuple(t for p in parts for t in p.type_seq)
-        mids = tuple(x for p in parts for x in p.members)
+        seq = tuple(chain.from_iterable([p.type_seq for p in parts]))
+        mids = tuple(chain.from_iterable([p.members for p in parts]))
         row = gcost[z].tolist()
         cost = {devices[k]: row[k] for k in range(D) if row[k] == row[k]}
         gid = min(p.id for p in parts)
