@@ -382,7 +382,8 @@ def run_ours(args):
                 "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan",
                 "issue_bound_evidence": ({k: tr[k] for k in ("ipc_active", "issue_slots_busy", "active_threads_per_warp",
                                                              "l2_hit_rate", "achieved_warps_per_sm") if k in tr}
-                                         if tr else None)}
+                                         if tr else None),
+                "shared_memory": (tr or {}).get("shared_memory")}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
