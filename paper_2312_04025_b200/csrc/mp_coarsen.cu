@@ -276,6 +276,7 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
         const int src = s0 + __ffs(srcs) - 1;
         int sp = 0;
         stack[sp++] = src;
+        __syncwarp();
         while (sp > 0) {
             int cur = s.where[stack[--sp]];
             // independent loads of cur's record, issued together
@@ -310,6 +311,7 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 const int sv = lane < lc ? s.seq[static_cast<size_t>(cur) * Lmax + lane] : from_n;
                 const int h_cur = s.head[cur], t_cur = s.tail[cur], h_nxt = s.head[nxt], t_nxt = s.tail[nxt];
                 const int2 ob_nxt = s.obt[nxt];
+                __syncwarp();  // every lane has read cur's / nxt's records before any lane rewrites them
                 // rename the members of the group whose id disappears
                 if (nw == cur) {
                     for (int x = h_nxt;; x = s.next[x]) {

@@ -310,6 +310,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         const double wdur = __shfl_sync(kFull, bdur, src_lane);
         be = __shfl_sync(kFull, be, src_lane);  // lanes >= maxr skipped butterfly rounds
         const int last = nready - 1;
+        __syncwarp();  // every lane's scan reads precede the refill of the hole
         if (owner && bs != last) {  // unordered removal: move the last entry into the hole
             const double2 l0 = reinterpret_cast<const double2 *>(rdy + last)[0];
             const double2 l1 = reinterpret_cast<const double2 *>(rdy + last)[1];
@@ -372,9 +373,14 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const bool multi = k != MP_NONE;
             const uint32_t kc = multi ? k : 0;
             const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
-            const int np = static_cast<int>(m_np[kc]) - 1;
-            const double cur = m_est[kc];
-            const uint32_t ct = m_tie[kc];
+            int np = 0;  // predicated loads: only an active lane's own consumer is read
+            double cur = 0.0;
+            uint32_t ct = 0;
+            if (act && multi) {
+                np = static_cast<int>(m_np[kc]) - 1;
+                cur = m_est[kc];
+                ct = m_tie[kc];
+            }
             const bool up = end > cur;
             const double ej = multi ? (up ? end : cur) : end;
             const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
@@ -505,6 +511,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
                              : slot<double>(st, a.so.clk);
     unsigned char *devbuf = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) devbuf[i] = 0;
+    __syncwarp();  // zeroing (byte per lane) before the 16-byte row copies of other lanes
     double best_ms = kInf;
     long long best_row = LLONG_MAX;
     const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
@@ -603,6 +610,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
                              : slot<double>(st, a.so.clk);
     unsigned char *dev = st + a.so.dev;
     for (int i = gl; i < a.n_ops + 16; i += G) dev[i] = 0;
+    __syncwarp();
     const int n = a.n_ops, K = a.K;
     for (;;) {
         unsigned long long base = 0;
