@@ -265,9 +265,11 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         for (int s0 = 0; s0 < maxr; s0 += G) {
             const int s = s0 + gl;
             const bool valid = !done && s < nready;
-            const int sc = valid ? s : 0;  // slot arrays always hold >= 1 entry
-            const double2 h0 = reinterpret_cast<const double2 *>(rdy + sc)[0];
-            const double2 h1 = reinterpret_cast<const double2 *>(rdy + sc)[1];
+            double2 h0 = make_double2(0.0, 0.0), h1 = make_double2(0.0, 0.0);
+            if (valid) {  // predicated: lanes past the ready set issue no loads
+                h0 = reinterpret_cast<const double2 *>(rdy + s)[0];
+                h1 = reinterpret_cast<const double2 *>(rdy + s)[1];
+            }
             const uint32_t m = static_cast<uint32_t>(dbits(h1.y));
             const uint32_t tie = static_cast<uint32_t>(dbits(h1.y) >> 32);
             const unsigned long long es = dbits(h0.x);
@@ -354,7 +356,12 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const double2 rec = T_rec[q];
             const unsigned long long rb = dbits(rec.x);
             const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
-            const int dj = dev[j];
+            int dj = 0;
+            double rj = 0.0;
+            if (act) {  // predicated: idle lanes issue no state loads
+                dj = dev[j];
+                rj = rank[j];
+            }
             const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
             const bool cross = dj != d;
             const bool via_colo = COLO && isop && !cross;
@@ -364,7 +371,6 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const bool fcross = isop && cross;
             const int bi = fcross ? d * K + dj : 0;
             const double fdur = fcross ? div_bw(rec.y, T_bw[bi], T_rbw[bi], fast) : 0.0;
-            const double rj = rank[j];
             const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
                                                    (static_cast<uint32_t>(2 * K + dj) << 26))
                                                 : ((RZ << 20) | (RZ << 26)));
