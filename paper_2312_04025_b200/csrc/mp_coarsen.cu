@@ -380,7 +380,7 @@ __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const 
 // CTA), the DFS runs on warp 0 at shared-memory latency, and the state is
 // written back for the parallel final partition.
 __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int TN, const int *indeg, const int *obeg,
-                                                   const int *odst, Trie tg, DfsState sg, int stack_cap) {
+                                                   const int *odst, Trie tg, DfsState sg, int stack_cap, int *seen) {
     extern __shared__ __align__(16) int smi[];
     int *p = smi;
     auto take = [&](int n) {
@@ -430,6 +430,29 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
         t.type[i] = tg.type[i];
         t.flags[i] = tg.flags[i];
     }
+    __syncthreads();
+    // Kahn from the sources (graph.py:274-288) on the shared-memory CSR, level by
+    // level (stack = remaining in-degrees, buf = the queue); *seen < V means a cycle
+    __shared__ int s_tail;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) stack[i] = ind[i];
+    if (threadIdx.x == 0) s_tail = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < V; i += blockDim.x)
+        if (stack[i] == 0) buf[atomicAdd(&s_tail, 1)] = i;
+    __syncthreads();
+    for (int head = 0;;) {
+        const int tail = s_tail;
+        __syncthreads();  // every thread has this level's end before the level appends
+        if (head == tail) break;
+        for (int q0 = head + static_cast<int>(threadIdx.x); q0 < tail; q0 += blockDim.x) {
+            const int v = buf[q0];
+            for (int q = ob[v]; q < ob[v + 1]; ++q)
+                if (atomicSub(&stack[od[q]], 1) == 1) buf[atomicAdd(&s_tail, 1)] = od[q];
+        }
+        head = tail;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *seen = s_tail;
     __syncthreads();
     if (threadIdx.x < 32) dfs_run(V, Lmax, ind, ob, od, t, s, stack, buf);  // warp 0
     __syncthreads();
@@ -788,9 +811,15 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     }
     tb = tmpb;
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, outcnt, obeg, V + 1, st));
-    CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
-    k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, counters);
-    ++g_mp_launches;
+    // small graphs run Kahn inside the shared-memory DFS kernel (below)
+    const int stack_cap = E + V + 8;
+    const size_t dsm = dfs_smem_bytes(V, E, Lmax, TN, stack_cap);
+    const bool dfs_in_smem = dsm <= static_cast<size_t>(MP_SMEM_DYN_MAX);
+    if (!dfs_in_smem) {
+        CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
+        k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, counters);
+        ++g_mp_launches;
+    }
 
     // ---- trie + node states + K1b DFS ---------------------------------------------------
     Trie trie{};
@@ -809,21 +838,19 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     s.tag = ar.take<int>(V);
     s.obt = ar.take<int2>(V);
     s.visited = ar.take<unsigned char>(V);
-    const int stack_cap = E + V + 8;
     int *stack = ar.take<int>(stack_cap), *buf = ar.take<int>(stack_cap);
     int *ntrie = ar.take<int>(4);
     k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
     ++g_mp_launches;
     k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, obeg, s);
     ++g_mp_launches;
-    const size_t dsm = dfs_smem_bytes(V, E, Lmax, TN, stack_cap);
-    if (dsm <= static_cast<size_t>(MP_SMEM_DYN_MAX)) {
+    if (dfs_in_smem) {
         if (!cx.smem_attr) {
             CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs_smem),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
             cx.smem_attr = true;
         }
-        k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap);
+        k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap, counters);
     } else {
         // one thread walks an L2-resident state: give the SM's unified L1 its whole
         // capacity (no shared memory is used)
