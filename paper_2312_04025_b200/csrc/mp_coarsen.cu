@@ -122,7 +122,19 @@ struct DfsState {
     int *tag;       // [V] by group id
     int2 *obt;      // [V] by group id: out-edge range [obeg[tail], obeg[tail+1]) of the group's tail
     unsigned char *visited;  // [V] by group id
+    unsigned char *vl;       // [V] (large graphs, shared memory) visited << 7 | length, replacing
+                             //     `visited` and `len` inside the DFS (VL variant of dfs_run)
 };
+
+// visited flag / sequence length of group g (VL: one shared-memory byte for both)
+template <bool VL>
+__device__ __forceinline__ bool dfs_visited(const DfsState &s, int g) {
+    return VL ? (s.vl[g] >> 7) != 0 : s.visited[g] != 0;
+}
+template <bool VL>
+__device__ __forceinline__ int dfs_len(const DfsState &s, int g) {
+    return VL ? (s.vl[g] & 0x7f) : s.len[g];
+}
 
 // Initial per-node state: singleton groups with the node's own type sequence.
 __global__ void k_init_nodes(int V, int Lmax, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
@@ -226,6 +238,7 @@ struct OutSet {
     bool wide;      // out-degree > 32: the set is in buf[0..n) (scalar form)
 };
 
+template <bool VL>
 __device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *odst, int2 ob, int self, int *buf) {
     const int lane = threadIdx.x & 31;
     OutSet o;
@@ -233,7 +246,7 @@ __device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *
     if (o.wide) {
         o.n = out_groups(s, odst, ob, self, buf);
         o.one = buf[0];
-        o.one_len = o.n == 1 ? s.len[o.one] : 0;
+        o.one_len = o.n == 1 ? dfs_len<VL>(s, o.one) : 0;
         o.w = -1;
         o.lead = o.vis = false;
         return o;
@@ -242,8 +255,14 @@ __device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *
     bool vis = true;
     if (ob.x + lane < ob.y) {
         const int x = s.where[odst[ob.x + lane]];
-        vis = s.visited[x];  // x is a live group id even when it is `self`
-        lw = s.len[x];
+        if constexpr (VL) {  // x is a live group id even when it is `self`
+            const unsigned v = s.vl[x];
+            vis = (v >> 7) != 0;
+            lw = static_cast<int>(v & 0x7fu);
+        } else {
+            vis = s.visited[x];
+            lw = s.len[x];
+        }
         w = x == self ? -1 : x;
     }
     const unsigned same = __match_any_sync(0xffffffffu, w);
@@ -266,6 +285,7 @@ __device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *
 // sequence concatenation and the source scan.  Per DFS node the dependent
 // chain is stack -> where -> {visited, tail range, trie state, length} ->
 // successor -> its group -> {visited, length}.
+template <bool VL>
 __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, const Trie &t,
                         const DfsState &s, int *stack, int *buf) {
     const int lane = threadIdx.x & 31;
@@ -280,15 +300,15 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
         while (sp > 0) {
             int cur = s.where[stack[--sp]];
             // independent loads of cur's record, issued together
-            const bool seen = s.visited[cur];
+            const bool seen = dfs_visited<VL>(s, cur);
             int2 ob = s.obt[cur];
             int st_cur = s.state[cur];
-            int len_cur = s.len[cur];
+            int len_cur = dfs_len<VL>(s, cur);
             if (seen) continue;
             OutSet os;
             for (;;) {
                 // |out[cur]| == 1 ?  (fusion.py:291-294)
-                os = out_groups_warp(s, odst, ob, cur, buf);
+                os = out_groups_warp<VL>(s, odst, ob, cur, buf);
                 if (os.n != 1) break;
                 const int nxt = os.one;
                 // _match_seqs(seqs[cur], seqs[nxt]) (fusion.py:93-104) via the trie
@@ -328,7 +348,11 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.head[nw] = h_cur;
                 s.tail[nw] = t_nxt;
                 s.obt[nw] = ob_nxt;
-                s.len[nw] = L2;
+                if constexpr (VL) {
+                    s.vl[nw] = static_cast<unsigned char>((s.vl[nw] & 0x80u) | static_cast<unsigned>(L2));
+                } else {
+                    s.len[nw] = L2;
+                }
                 __syncwarp();
                 if (lane < L2) s.seq[static_cast<size_t>(nw) * Lmax + lane] = sv;
                 __syncwarp();
@@ -339,7 +363,11 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 st_cur = st;
                 len_cur = L2;
             }
-            s.visited[cur] = 1;
+            if constexpr (VL) {
+                s.vl[cur] = static_cast<unsigned char>(s.vl[cur] | 0x80u);
+            } else {
+                s.visited[cur] = 1;
+            }
             // push unvisited out groups in descending id (fusion.py:301-303)
             if (!os.wide) {
                 // position of a pushed group = number of pushed groups above it
@@ -364,16 +392,28 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 buf[j + 1] = v;
             }
             for (int z = no - 1; z >= 0; --z)
-                if (!s.visited[buf[z]]) stack[sp++] = buf[z];
+                if (!dfs_visited<VL>(s, buf[z])) stack[sp++] = buf[z];
         }
         }
     }
 }
 
 __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
-                      int *stack, int *buf) {
+                      int *stack, int *buf,
+                      int use_vl) {
     if (threadIdx.x >= 32 || blockIdx.x != 0) return;
-    dfs_run(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
+    if (!use_vl) {
+        dfs_run<false>(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
+        return;
+    }
+    // visited flags and lengths (<= Lmax + 1 <= 31) in one shared-memory byte per group
+    extern __shared__ unsigned char vl_sm[];
+    DfsState q = s;
+    q.vl = vl_sm;
+    for (int i = threadIdx.x; i < V; i += 32) vl_sm[i] = static_cast<unsigned char>(s.len[i]);
+    __syncwarp();
+    dfs_run<true>(V, Lmax, indeg, obeg, odst, t, q, stack, buf);
+    // len is read again only by this kernel; visited not at all after it
 }
 
 // Small graphs: the whole DFS state, CSR and trie move into shared memory (one
@@ -389,6 +429,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
         return r;
     };
     DfsState s;
+    s.vl = nullptr;
     s.where = take(V);
     s.next = take(V);
     s.head = take(V);
@@ -454,7 +495,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
     }
     if (threadIdx.x == 0) *seen = s_tail;
     __syncthreads();
-    if (threadIdx.x < 32) dfs_run(V, Lmax, ind, ob, od, t, s, stack, buf);  // warp 0
+    if (threadIdx.x < 32) dfs_run<false>(V, Lmax, ind, ob, od, t, s, stack, buf);  // warp 0
     __syncthreads();
     for (int i = threadIdx.x; i < V; i += blockDim.x) {
         sg.where[i] = s.where[i];
@@ -852,14 +893,16 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
         }
         k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap, counters);
     } else {
-        // one thread walks an L2-resident state: give the SM's unified L1 its whole
-        // capacity (no shared memory is used)
+        // one warp walks an L2-resident state; the visited flags and lengths (one byte
+        // per group) sit in shared memory when they fit, the rest of the SM's unified
+        // L1 caches the state
+        const bool use_vl = static_cast<size_t>(V) <= static_cast<size_t>(MP_SMEM_DYN_MAX);
         if (!cx.dfs_attr) {
             CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs),
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
             cx.dfs_attr = true;
         }
-        k_dfs<<<1, 32, 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf);
+        k_dfs<<<1, 32, use_vl ? V : 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf, use_vl ? 1 : 0);
     }
     ++g_mp_launches;
 
