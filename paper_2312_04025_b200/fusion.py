@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import sys
 from itertools import chain
+from operator import attrgetter
 from dataclasses import dataclass
 from enum import Enum
 from typing import Iterable, Iterator
@@ -111,6 +112,10 @@ _TAG_CODE = {Tag.PLAIN: 0, Tag.FUSED: 1, Tag.BOUND: 2}
 _CODE_TAG = {0: Tag.PLAIN, 1: Tag.FUSED, 2: Tag.BOUND}
 
 
+_A_SEQ, _A_TAG, _A_MEM, _A_CT = (attrgetter("type_seq"), attrgetter("tag"), attrgetter("mem_bytes"),
+                                  attrgetter("compute_time"))
+
+
 class _Flat:
     """Array form of a coarsening problem (mp_coarsen_input)."""
 
@@ -118,7 +123,7 @@ class _Flat:
         nodes = g.nodes
         dg = g.csr()
         V = len(nodes)
-        seqs = [n.type_seq for n in nodes]
+        seqs = list(map(_A_SEQ, nodes))
         flat_types = list(chain.from_iterable(seqs))
         for r in rules:
             flat_types.extend(r.pattern)
@@ -130,13 +135,14 @@ class _Flat:
         seq_beg = np.zeros(V + 1, np.int32)
         np.cumsum(lens, out=seq_beg[1:])
         total = int(seq_beg[-1])
-        seq = np.fromiter((types[t] for t in flat_types[:total]), dtype=np.int32, count=total)
-        tag = np.fromiter((_TAG_CODE[n.tag] for n in nodes), dtype=np.int32, count=V)
-        mem = np.fromiter((n.mem_bytes for n in nodes), dtype=np.int64, count=V)
-        cts = [n.compute_time for n in nodes]
+        seq = np.fromiter(map(types.__getitem__, flat_types[:total]), dtype=np.int32, count=total)
+        tag = np.fromiter(map(_TAG_CODE.__getitem__, map(_A_TAG, nodes)), dtype=np.int32, count=V)
+        mem = np.fromiter(map(_A_MEM, nodes), dtype=np.int64, count=V)
+        cts = list(map(_A_CT, nodes))
         devs = set()
-        first = tuple(cts[0]) if cts else ()
-        uniform = all(tuple(ct) == first for ct in cts)
+        keys = list(map(tuple, cts))
+        first = keys[0] if keys else ()
+        uniform = keys.count(first) == len(keys)
         if uniform:
             devs.update(first)
         else:
