@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import CycleCreationError, CycleError, UnknownEdgeError
-from .graph import CompGraph, FlowEdge, OpNode, Tag, _make_edge, _make_opnode, find_cycle, validate_dag
+from .graph import CompGraph, FlowEdge, OpNode, Tag, _bulk_objects, _make_edge, _make_opnode, find_cycle, validate_dag
 from .profiles import CostOverrides
 
 FUSE_JOINER = "∘"  # joins member types in a fused node's op_type (fusion.py:23)
@@ -202,7 +202,8 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
     """
     if len(g) == 0:
         return CompGraph([], [])
-    flat = _Flat(g, rules, overrides)
+    with _bulk_objects():
+        flat = _Flat(g, rules, overrides)
     out = N.mp_coarsen_output()
     err = N.mp_error()
     lib = N.lib()
@@ -215,7 +216,6 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         nodes_in = g.nodes
         ng, ne = out.n_groups, out.n_edges
         D = len(flat.devices)
-        grp_node = np.ctypeslib.as_array(out.grp_node, (ng,)).copy() if ng else np.zeros(0, np.int32)
         grp_tag = np.ctypeslib.as_array(out.grp_tag, (ng,)).copy() if ng else np.zeros(0, np.int32)
         mbeg = np.ctypeslib.as_array(out.mem_beg, (ng + 1,)).copy()
         members = np.ctypeslib.as_array(out.members, (int(mbeg[-1]),)).copy() if mbeg[-1] else np.zeros(0, np.int32)
@@ -227,27 +227,43 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         epay = np.ctypeslib.as_array(out.out_payload, (ne,)).copy() if ne else np.zeros(0, np.int64)
     finally:
         lib.mp_coarsen_free(C.byref(out))
+    with _bulk_objects():
+        return _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay)
+
+
+def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay) -> CompGraph:
+    """The coarsened CompGraph from the native output arrays (node by node as the
+    reference builds it; unfused nodes are the input objects themselves)."""
     new_nodes = []
-    gid_of = []
-    sizes = np.diff(mbeg)
     mb = mbeg.tolist()
     mlist = members.tolist()
     devices = flat.devices
+    cost_rows = gcost.tolist()
+    partial = np.isnan(gcost).any(axis=1).tolist() if ng else []  # a device some member lacks
+    mem_l = gmem.tolist()
+    tag_l = grp_tag.tolist()
+    join = FUSE_JOINER.join
     for z in range(ng):
-        if sizes[z] == 1:
-            n = nodes_in[mlist[mb[z]]]
-            new_nodes.append(n)
-            gid_of.append(n.id)
+        b, e = mb[z], mb[z + 1]
+        if e - b == 1:
+            new_nodes.append(nodes_in[mlist[b]])
             continue
-        parts = [nodes_in[m] for m in mlist[mb[z]:mb[z + 1]]]
-        seq = tuple(chain.from_iterable([p.type_seq for p in parts]))
-        mids = tuple(chain.from_iterable([p.members for p in parts]))
-        row = gcost[z].tolist()
-        cost = {devices[k]: row[k] for k in range(D) if row[k] == row[k]}
-        gid = min(p.id for p in parts)
-        new_nodes.append(_make_opnode(gid, FUSE_JOINER.join(seq), int(gmem[z]), cost, mids, seq,
-                                      _CODE_TAG[int(grp_tag[z])]))
-        gid_of.append(gid)
+        if e - b == 2:
+            p0, p1 = nodes_in[mlist[b]], nodes_in[mlist[b + 1]]
+            seq = p0.type_seq + p1.type_seq
+            mids = p0.members + p1.members
+            gid = p0.id if p0.id < p1.id else p1.id
+        else:
+            idx = mlist[b:e]
+            parts = [nodes_in[m] for m in idx]
+            seq = tuple(chain.from_iterable([p.type_seq for p in parts]))
+            mids = tuple(chain.from_iterable([p.members for p in parts]))
+            # nodes_in is in ascending id order: the smallest member index has the smallest id
+            gid = nodes_in[min(idx)].id
+        row = cost_rows[z]
+        cost = ({devices[k]: row[k] for k in range(D) if row[k] == row[k]} if partial[z]
+                else dict(zip(devices, row)))
+        new_nodes.append(_make_opnode(gid, join(seq), mem_l[z], cost, mids, seq, _CODE_TAG[tag_l[z]]))
     # output nodes come in ascending id order, so group indices are node indices
     return CompGraph._from_arrays(new_nodes, esrc, edst, epay)
 
