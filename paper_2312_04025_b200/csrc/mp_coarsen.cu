@@ -297,8 +297,18 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
         int sp = 0;
         stack[sp++] = src;
         __syncwarp();
+        int top = -1;  // the group just pushed on top of the stack, if any
         while (sp > 0) {
-            int cur = s.where[stack[--sp]];
+            // a group pushed by the previous step is still a live group id (nothing
+            // merged since), so where[top] == top: skip the stack and where loads
+            int cur;
+            if (VL && top >= 0) {  // (global-memory replay only: shared-memory loads are cheap)
+                --sp;
+                cur = top;
+                top = -1;
+            } else {
+                cur = s.where[stack[--sp]];
+            }
             // independent loads of cur's record, issued together
             const bool seen = dfs_visited<VL>(s, cur);
             int2 ob = s.obt[cur];
@@ -377,6 +387,8 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 for (unsigned m = P; m; m &= m - 1u) above += __shfl_sync(0xffffffffu, os.w, __ffs(m) - 1) > os.w;
                 if (push) stack[sp + above] = os.w;
                 sp += __popc(P);
+                // the smallest pushed group lands on top and is popped next
+                if (VL && P) top = __reduce_min_sync(0xffffffffu, push ? os.w : 0x7fffffff);
                 __syncwarp();
                 continue;
             }

@@ -211,3 +211,29 @@ def test_mip_start_names_and_values_follow_the_reference_model():
         mdl = opplace.build_model(rg, rc, opplace.effective_bandwidth(rc))
         names = {v.name for v in mdl.vars}
         assert set(vals) <= names
+
+
+def test_bulk_object_construction_restores_the_collector():
+    """The GC pause around bulk OpNode creation (gcof, load_graph) restores the
+    collector's previous state, also when the body raises."""
+    import gc
+
+    from paper_2312_04025_b200.graph import _bulk_objects
+
+    assert gc.isenabled()
+    with _bulk_objects():
+        assert not gc.isenabled()
+    assert gc.isenabled()
+    try:
+        with _bulk_objects():
+            raise ValueError("boom")
+    except ValueError:
+        pass
+    assert gc.isenabled()
+    gc.disable()
+    try:
+        with _bulk_objects():
+            pass
+        assert not gc.isenabled()
+    finally:
+        gc.enable()
