@@ -13,7 +13,10 @@
 //                  a multi-input consumer, and whether a consumer had already
 //                  extended itself when absorbed, depend on the lexicographic DFS
 //                  order — a P-complete order in general — so this phase replays
-//                  the DFS exactly, on one GPU thread, over compact state.
+//                  the DFS exactly, on one warp (lanes split each step's successor
+//                  gathers), over compact state: in one CTA's shared memory with
+//                  Kahn's check fused for small graphs, else from L1/L2 with the
+//                  visited flags and lengths in shared memory.
 //                  No out/inn sets are kept: a group's quotient out-set is the
 //                  set of current groups of its tail member's input successors
 //                  (App. B: out(combine(a, b)) = out(b)), and the rule match is a
