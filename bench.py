@@ -253,7 +253,13 @@ def run_ours(args):
     w = build_workload(args.workload)
     t0 = time.perf_counter()
     coarse = mp.gcof(w.raw, w.rules, device=local)
-    t_gcof = time.perf_counter() - t0
+    t_gcof = time.perf_counter() - t0  # first call: includes the coarsening context's allocations
+    t_warm = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        mp.gcof(w.raw, w.rules, device=local)
+        t_warm.append(time.perf_counter() - t0)
+    t_gcof_warm = sorted(t_warm)[len(t_warm) // 2]
     inst = mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster), device=local)
     if args.tune:
         G, U, rc = (int(x) for x in (args.tune.split(":") + ["0", "0"])[:3])
@@ -394,7 +400,7 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 ({P * n_ops / 1e6:.0f} MB per GPU per step)",
                        "shape": {k: info[k] for k in ("group_lanes", "lanes_used", "groups_per_cta", "ctas",
                                                        "ready_cap", "colo", "onchip", "smem_bytes")},
-                       "gcof_ms": t_gcof * 1e3},
+                       "gcof_ms": t_gcof_warm * 1e3, "gcof_first_call_ms": t_gcof * 1e3},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": P * n_ops, "d2h_bytes_per_step": P * 8 + 16},
             "gpu_launches": int(launches),
             "roofline": roof,
