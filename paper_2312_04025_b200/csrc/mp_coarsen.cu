@@ -732,6 +732,9 @@ struct CoarsenCtx {
     size_t pin_cap = 0;
     bool smem_attr = false;
     bool dfs_attr = false;
+    // large graphs: Kahn's cycle check runs on a side stream beside the DFS (both one CTA)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 CoarsenCtx g_ctx[64];
 
@@ -768,6 +771,9 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     CK(cudaSetDevice(device));
     if (!cx.st) CK(cudaStreamCreateWithFlags(&cx.st, cudaStreamNonBlocking));
     cudaStream_t st = cx.st;
+    // a previous call that returned early may have left Kahn running on the side
+    // stream over this context's arena
+    if (cx.side) CK(cudaStreamWaitEvent(st, cx.ev_join, 0));
     const int TN = R * Lmax + 2;
 
     // ---- one packed upload through pinned staging ---------------------------------
@@ -871,10 +877,20 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     const int stack_cap = E + V + 8;
     const size_t dsm = dfs_smem_bytes(V, E, Lmax, TN, stack_cap);
     const bool dfs_in_smem = dsm <= static_cast<size_t>(MP_SMEM_DYN_MAX);
+    // large graphs: Kahn on a side stream, concurrent with the DFS that follows on `st`
+    // (it only reads the CSR and in-degrees; its count is joined before the download)
     if (!dfs_in_smem) {
-        CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
-        k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, counters);
+        if (!cx.side) {
+            CK(cudaStreamCreateWithFlags(&cx.side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&cx.ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&cx.ev_join, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(cx.ev_fork, st));
+        CK(cudaStreamWaitEvent(cx.side, cx.ev_fork, 0));
+        CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, cx.side));
+        k_kahn<<<1, 1024, 0, cx.side>>>(V, obeg, odst, deg, fa, fb, counters);
         ++g_mp_launches;
+        CK(cudaEventRecord(cx.ev_join, cx.side));
     }
 
     // ---- trie + node states + K1b DFS ---------------------------------------------------
@@ -963,6 +979,8 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
         return cset_err(err, MP_ERR_UNSUPPORTED, static_cast<int64_t>(ar.used), static_cast<int64_t>(ar.cap),
                         "internal arena overflow");
     CK(cudaGetLastError());
+
+    if (!dfs_in_smem) CK(cudaStreamWaitEvent(st, cx.ev_join, 0));  // Kahn's count
 
     // ---- one packed download -------------------------------------------------------------
     size_t q = 0;

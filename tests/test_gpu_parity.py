@@ -133,6 +133,19 @@ def test_gcof_rejects_cycles_and_is_idempotent():
             assert mp.gcof(out, rules_from(case["rules"])) == out
 
 
+def test_gcof_rejects_cycles_on_large_graphs():
+    """Past the shared-memory size the cycle check runs beside the DFS on a side
+    stream; a back edge in a 20k-op graph must still raise CycleError, and the
+    context must stay usable afterwards."""
+    rules = workloads.table_rules()
+    g = mp.gen_synthetic(mp.GenSpec(ops=20_000, width=32, density=0.5, devices=(0, 1)), 3)
+    e = g.edges[len(g.edges) // 2]
+    cyc = mp.CompGraph(g.nodes, list(g.edges) + [mp.FlowEdge(e.dst, e.src, 8)])  # a 2-cycle
+    with pytest.raises(mp.CycleError):
+        mp.gcof(cyc, rules)
+    assert len(mp.gcof(g, rules)) < len(g)
+
+
 def test_gcof_large_synthetic_vs_oracle(oracle_mod):
     from paper_2312_04025_b200.fusion import _Flat
 
