@@ -361,8 +361,8 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.head[nw] = h_cur;
                 s.tail[nw] = t_nxt;
                 s.obt[nw] = ob_nxt;
-                if constexpr (VL) {
-                    s.vl[nw] = static_cast<unsigned char>((s.vl[nw] & 0x80u) | static_cast<unsigned>(L2));
+                if constexpr (VL) {  // read-modify-write: one lane (the __syncwarp below publishes it)
+                    if (lane == 0) s.vl[nw] = static_cast<unsigned char>((s.vl[nw] & 0x80u) | static_cast<unsigned>(L2));
                 } else {
                     s.len[nw] = L2;
                 }
@@ -377,7 +377,8 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 len_cur = L2;
             }
             if constexpr (VL) {
-                s.vl[cur] = static_cast<unsigned char>(s.vl[cur] | 0x80u);
+                if (lane == 0) s.vl[cur] = static_cast<unsigned char>(s.vl[cur] | 0x80u);
+                __syncwarp();
             } else {
                 s.visited[cur] = 1;
             }

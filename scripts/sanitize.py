@@ -38,4 +38,6 @@ print("bnb", sol.status, sol.objective_s, flush=True)
 s = mp.greedy_place(g, w.cluster, bw)
 print("greedy", s.makespan_s, flush=True)
 print("audit", len(mp.check_feasibility(s, g, w.cluster, bw)), flush=True)
+big = mp.gen_synthetic(mp.GenSpec(ops=15_000, width=32, density=0.5, devices=(0, 1)), 2)
+print("gcof 15k (global DFS, side-stream Kahn)", len(mp.gcof(big, workloads.table_rules())), flush=True)
 print("done", flush=True)
