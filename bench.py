@@ -1,20 +1,28 @@
 #!/usr/bin/env python3
 """Headline benchmark: candidate placements evaluated per second (makespan).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2k8]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
 
-Workload (BASELINE.json configs[1]): the BERT-large inference graph (embed + 24
-encoder layers, 481 raw ops) coarsened by GCOF on the GPU to 265 ops / 360
-flows, placed on the Table-III intra-server cluster (V100, V100, P100, P100).
-A step evaluates one batch of ROWS random placements per GPU (uint8 device
-indices from PCG64(2 + 1000*rank): weak scaling, each rank a disjoint shard)
-and reduces the best placement across GPUs (16-byte NCCL all-gather of
-(makespan bits, global row)).  Inputs are 278 MB per GPU per step (> L2).
+``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks; asking for more GPUs than the box has is
+an error (exit 2), never a silent one-rank run.
+
+Workload (BASELINE.json north star: "BERT-large 8-device config"): the BERT-large
+inference graph (embed + 24 encoder layers, 481 raw ops) coarsened by GCOF on the
+GPU to 265 ops / 360 flows, placed on two Table-III intra-server quads joined by
+100 Gb/s InfiniBand (K=8).  A step evaluates one batch of
+ROWS random placements per GPU (uint8 device indices from PCG64(2 + 1000*rank):
+weak scaling, each rank a disjoint shard) and reduces the best placement across
+GPUs (16-byte NCCL all-gather of (makespan bits, global row)).  Inputs are
+278 MB per GPU per step (> L2).  ``--workload c2`` is the K=4 quad (configs[1]).
 
 value  = device-resident throughput: rows already in HBM, max time over ranks.
 e2e    = the same step through the C ABI with HOST (pinned) buffers: H2D of the
          rows and D2H of every makespan inside the timed region.
+parity = after timing, every makespan and status of rank 0's last step is
+         compared bit for bit with the CPU oracle (oracle/moirai_oracle.c), and
+         the argmin with the oracle's first strict minimum.
 Reference arm (--impl reference): the reference algorithm in pure Python
 (oracle/pyref.py, faithful to opplace._schedule) on every host core.
 """
@@ -23,8 +31,10 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,6 +49,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "candidate placements evaluated/sec (makespan) at 1/2/4/8 B200 vs host-CPU ref"
 UNIT = "placements/s"
+WORKLOADS = ("c1", "c2", "c2k8", "c3", "c4", "c4pcie")
 
 
 def log(*a):
@@ -52,12 +63,20 @@ def dist_env():
     return world, rank, local
 
 
-# ---- workload (built identically on every rank) ------------------------------------------
+# ---- workload (built identically on every rank and in both arms) ---------------------------
 def build_workload(name: str):
     from paper_2312_04025_b200 import workloads
 
     return {"c1": workloads.c1, "c2": lambda: workloads.c2(4), "c2k8": lambda: workloads.c2(8),
-            "c3": workloads.c3, "c4": workloads.c4}[name]()
+            "c3": workloads.c3, "c4": workloads.c4, "c4pcie": lambda: workloads.c4("pcie")}[name]()
+
+
+def workload_config(w, n_ops: int, n_flows: int, K: int) -> dict:
+    """The `config` object of the JSON line — identical in both arms."""
+    return {"workload": f"{w.name} (GCOF {len(w.raw)} -> {n_ops} ops / {n_flows} flows, K={K})",
+            "placements": "PCG64(seed=2+1000*rank) uint8 device indices per op, one row per placement",
+            "l2": "inputs larger than L2 (265 B x 2^20 rows = 278 MB per GPU per step)",
+            "dtype_note": "fp64 makespans, bit-exact with the reference"}
 
 
 def coarse_on_cpu(w):
@@ -108,12 +127,9 @@ def cpu_baseline_python(arrays, rows_all, seconds: float):
                       f"opplace._schedule (oracle/pyref.py), {procs} processes, {dt:.1f} s"}
 
 
-def cpu_baseline_native(arrays, rows_all, seconds: float):
+def cpu_baseline_native(orc, rows_all, seconds: float):
     """The C restatement (oracle/moirai_oracle.c) on every host core — a far
     stronger CPU baseline than the reference's own Python, reported alongside."""
-    from oracle.oracle import OracleInstance
-
-    orc = OracleInstance(*arrays)
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
     orc.eval_batch(rows_all[:2000], threads=cores)
@@ -124,6 +140,42 @@ def cpu_baseline_native(arrays, rows_all, seconds: float):
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"first {n} placements, C restatement (oracle/moirai_oracle.c), {cores} pthreads, {dt:.1f} s"}
+
+
+# ---- parity self-check (outside every timed region) -----------------------------------------
+def parity_check(orc, rows, ms, st, best_row, best_ms, budget_s: float = 60.0) -> dict:
+    """Bitwise comparison of the GPU's makespans/statuses with the C oracle on the
+    same rows, plus the keep-best row (brute_force's first strict minimum,
+    solver.py:277-279).  All rows when the oracle finishes within `budget_s`,
+    else a 4096-row sample that includes the argmin row."""
+    cores = os.cpu_count() or 1
+    P = len(rows)
+    t0 = time.perf_counter()
+    orc.eval_batch(rows[:256], threads=cores)
+    per = max((time.perf_counter() - t0) / 256, 1e-9)
+    if per * P <= budget_s:
+        idx = np.arange(P)
+    else:
+        idx = np.unique(np.concatenate([np.linspace(0, P - 1, 4096).astype(np.int64),
+                                        [best_row] if best_row >= 0 else []]).astype(np.int64))
+    want_ms, want_st = orc.eval_batch(np.ascontiguousarray(rows[idx]), threads=cores)
+    got_st = st[idx].astype(np.int64)
+    feas = want_st == 0
+    mism = int(np.count_nonzero(got_st != want_st.astype(np.int64)))
+    mism += int(np.count_nonzero(ms[idx][feas].view(np.uint64) != want_ms[feas].view(np.uint64)))
+    out = {"checked": int(len(idx)), "mismatches": mism, "oracle": "oracle/moirai_oracle.c",
+           "feasible": int(np.count_nonzero(feas)), "seconds": round(time.perf_counter() - t0, 2)}
+    if len(idx) == P:
+        if np.any(feas):
+            fi = np.flatnonzero(feas)
+            o_best = int(fi[np.argmin(want_ms[fi])])  # argmin returns the first minimum
+            out["argmin_row"] = o_best
+            out["argmin_match"] = bool(o_best == best_row and want_ms[o_best] == best_ms)
+        else:
+            out["argmin_match"] = best_row < 0
+    else:
+        out["argmin_match"] = bool(best_row < 0 or ms[best_row] == best_ms)
+    return out
 
 
 # ---- clocks ------------------------------------------------------------------------------
@@ -168,61 +220,68 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def measured_peak():
+# ---- roofline denominators ------------------------------------------------------------------
+def measured_hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         try:
-            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json, copy)"
         except Exception:
             pass
-    return 6650.0, "fallback"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    p = ROOT / "profiles" / "ncu_eval_traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text())
-        except Exception:
+def onchip_peaks() -> dict | None:
+    """Shared-memory and L2 load bandwidth measured on this box now
+    (paper_2312_04025_b200/csrc/mp_peaks.cu), before the timed region."""
+    lib_path = ROOT / "paper_2312_04025_b200" / "libmoirai_peaks.so"
+    if not lib_path.exists():
+        return None
+    lib = C.CDLL(str(lib_path))
+    out = (C.c_double * 3)()
+    res = {}
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    best = None
+    for width in (16, 8):
+        if lib.mp_peak_smem(width, 5, out) != 0:
             return None
-    return None
+        if best is None or out[0] > best[0]:
+            best = (out[0], out[1], width)
+    res["smem_TBps"] = best[0] / 1e12
+    res["smem_bytes_per_clk_per_sm"] = best[1]
+    res["smem_load_width"] = best[2]
+    res["sms"] = int(out[2])
+    if lib.mp_peak_l2(48, 5, out) != 0:
+        return None
+    res["l2_TBps"] = out[0] / 1e12
+    res["l2_buffer_mb"] = 48
+    res["clocks"] = clocks.stop()
+    res["source"] = "paper_2312_04025_b200/csrc/mp_peaks.cu (ld.shared.v4/v2 conflict-free, ld.global.cg over 48 MB)"
+    return res
 
 
-def north_star_config(P: int) -> dict:
-    """The BASELINE north-star target names the BERT-large 8-device config: same graph
-    on the K=8 cluster (two Table-III quads over 100 Gb/s), device-resident, this GPU."""
-    import torch
+def source_hash() -> str:
+    h = hashlib.sha256()
+    for p in sorted((ROOT / "paper_2312_04025_b200" / "csrc").glob("*")):
+        if p.suffix in (".cu", ".cuh", ".cpp"):
+            h.update(p.name.encode())
+            h.update(p.read_bytes())
+    h.update((ROOT / "include" / "moirai_b200.h").read_bytes())
+    return h.hexdigest()[:16]
 
-    import paper_2312_04025_b200 as mp
-    from paper_2312_04025_b200 import workloads
 
-    w = build_workload("c2k8")
-    coarse = mp.gcof(w.raw, w.rules)
-    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
-        rows = torch.from_numpy(workloads.placements(w.seed, P, inst.n_ops, inst.K)).cuda()
-        from paper_2312_04025_b200 import _native as N
-        import ctypes as C
-
-        lib, err, best, bms = N.lib(), N.mp_error(), C.c_int64(), C.c_double()
-        stream = torch.cuda.current_stream()
-
-        def step():
-            N.check(lib.mp_evaluate_argmin(inst.handle, C.c_void_p(rows.data_ptr()), P, None, None, C.byref(best),
-                                           C.byref(bms), N.MP_DEVICE_PTRS, C.c_void_p(stream.cuda_stream),
-                                           C.byref(err)), err)
-
-        for _ in range(3):
-            step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(5):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return {"workload": w.name + f" ({inst.n_ops} ops / {inst.n_flows} flows, K={inst.K})",
-                "value": 5 * P / (e0.elapsed_time(e1) / 1e3), "unit": UNIT, "steps": 5,
-                "note": "device-resident, 1 GPU; the driver's scaling run multiplies the headline config"}
+def ncu_summary(workload: str) -> dict | None:
+    """ncu metrics of the headline kernel for THIS source tree (profiles/r02/ncu_<workload>.json,
+    written by scripts/ncu_summary.py); ignored when its source hash differs (stale)."""
+    p = ROOT / "profiles" / "r02" / f"ncu_{workload}.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+    except Exception:
+        return None
+    d["current"] = d.get("source_hash") == source_hash()
+    return d
 
 
 # ---- our arm -----------------------------------------------------------------------------
@@ -235,6 +294,10 @@ def run_ours(args):
     from paper_2312_04025_b200 import workloads
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < (local + 1):
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, the box has {torch.cuda.device_count()} GPU(s)")
     torch.cuda.set_device(local)
     # under torchrun the NCCL group is always formed (also at N=1, so the collective
     # path is the one timed on every N)
@@ -250,6 +313,7 @@ def run_ours(args):
             sys.stdout.flush()
             os.dup2(saved, 1)
             os.close(saved)
+    peaks = onchip_peaks() if rank == 0 else None
     w = build_workload(args.workload)
     t0 = time.perf_counter()
     coarse = mp.gcof(w.raw, w.rules, device=local)
@@ -266,7 +330,7 @@ def run_ours(args):
         inst.tune(G, 0, rc, True, U)
     info = inst.info()
     P = args.rows
-    n_ops = inst.n_ops
+    n_ops, n_flows = inst.n_ops, inst.n_flows
     rows = workloads.placements(w.seed + 1000 * rank, P, n_ops, inst.K)
     h_rows = torch.from_numpy(rows).pin_memory()
     d_rows = h_rows.cuda()
@@ -293,12 +357,11 @@ def run_ours(args):
             return combine_records(gather_out.cpu().numpy())
         return combine_records(gather_in.cpu().numpy())
 
-    def step_device():
+    def launch_device():
         code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(d_rows.data_ptr()), P, C.c_void_p(d_ms.data_ptr()),
                                       C.c_void_p(d_st.data_ptr()), C.byref(best), C.byref(bms), N.MP_DEVICE_PTRS,
                                       C.c_void_p(stream.cuda_stream), C.byref(err))
         N.check(code, err, "mp_evaluate_argmin")
-        return exchange()
 
     def step_host():
         code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(h_rows.data_ptr()), P, C.c_void_p(h_ms.data_ptr()),
@@ -320,7 +383,8 @@ def run_ours(args):
         return float(t.item())
 
     for _ in range(args.warmup):
-        step_device()
+        launch_device()
+        exchange()
     # ---- timed region: device-resident -------------------------------------------------
     clocks = ClockSampler(local) if rank == 0 else None
     barrier()
@@ -334,10 +398,7 @@ def run_ours(args):
         k0 = torch.cuda.Event(enable_timing=True)
         k1 = torch.cuda.Event(enable_timing=True)
         k0.record(stream)
-        code = lib.mp_evaluate_argmin(inst.handle, C.c_void_p(d_rows.data_ptr()), P, C.c_void_p(d_ms.data_ptr()),
-                                      C.c_void_p(d_st.data_ptr()), C.byref(best), C.byref(bms), N.MP_DEVICE_PTRS,
-                                      C.c_void_p(stream.cuda_stream), C.byref(err))
-        N.check(code, err)
+        launch_device()
         k1.record(stream)
         result = exchange()
         kern_ms.append((k0, k1))
@@ -348,6 +409,9 @@ def run_ours(args):
     t_dev = max_over_ranks(e_start.elapsed_time(e_end) / 1e3)
     t_kern = statistics.mean(a.elapsed_time(b) / 1e3 for a, b in kern_ms)
     value = world * P * args.steps / t_dev
+    dev_ms = d_ms.cpu().numpy()
+    dev_st = d_st.cpu().numpy()
+    dev_best = (best.value, bms.value)
 
     # ---- e2e: host buffers through the C ABI --------------------------------------------
     for _ in range(max(1, args.warmup // 2)):
@@ -359,7 +423,7 @@ def run_ours(args):
     barrier()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     e2e = world * P * args.steps / t_e2e
-    assert np.array_equal(h_ms.numpy().view(np.uint64), d_ms.cpu().numpy().view(np.uint64)), "host/device mismatch"
+    assert np.array_equal(h_ms.numpy().view(np.uint64), dev_ms.view(np.uint64)), "host/device mismatch"
 
     # ---- local search throughput (secondary, untimed by the driver) ----------------------
     ls = None
@@ -377,50 +441,78 @@ def run_ours(args):
 
     out = None
     if rank == 0:
-        peak, peak_kind = measured_peak()
-        bytes_per = n_ops + 8  # one uint8 device id per op in, one fp64 makespan out (SURVEY §8(d) B_hbm)
-        achieved = P * bytes_per / t_kern / 1e9
-        tr = ncu_traffic()
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": (tr["dram_bytes_per_row"] * P if tr and "dram_bytes_per_row" in tr else None),
-                "traffic_source": (tr or {}).get("source"), "peak_source": peak_kind,
-                "algorithmic_bytes_per_placement": bytes_per, "kernel_ms": t_kern * 1e3,
-                "note": "issue/latency-bound fp64 list scheduling; HBM bytes are the algorithmic row+makespan",
-                "issue_bound_evidence": ({k: tr[k] for k in ("ipc_active", "issue_slots_busy", "active_threads_per_warp",
-                                                             "l2_hit_rate", "achieved_warps_per_sm") if k in tr}
-                                         if tr else None),
-                "shared_memory": (tr or {}).get("shared_memory")}
+        from oracle.oracle import OracleInstance
+
+        orc = OracleInstance(*inst._arrays)
+        parity = parity_check(orc, rows, dev_ms, dev_st, dev_best[0], dev_best[1])
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name + f" (GCOF {len(w.raw)} -> {n_ops} ops / {inst.n_flows} flows, K={inst.K})",
-                       "rows_per_gpu": P, "global_rows_per_step": P * world, "parallelism": f"dp{world} (row shards)",
-                       "placements": "PCG64(seed=2+1000*rank) uint8 device indices",
-                       "l2": f"inputs larger than L2 ({P * n_ops / 1e6:.0f} MB per GPU per step)",
-                       "shape": {k: info[k] for k in ("group_lanes", "lanes_used", "groups_per_cta", "ctas",
-                                                       "ready_cap", "colo", "onchip", "smem_bytes")},
-                       "gcof_ms": t_gcof_warm * 1e3, "gcof_first_call_ms": t_gcof * 1e3},
+            "config": workload_config(w, n_ops, n_flows, inst.K),
+            "rows_per_gpu": P, "global_rows_per_step": P * world, "parallelism": f"dp{world} (row shards)",
+            "shape": {k: info[k] for k in ("group_lanes", "lanes_used", "groups_per_cta", "ctas", "ready_cap", "colo",
+                                           "onchip", "smem_bytes") if k in info},
+            "gcof_ms": t_gcof_warm * 1e3, "gcof_first_call_ms": t_gcof * 1e3,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": P * n_ops, "d2h_bytes_per_step": P * 8 + 16},
             "gpu_launches": int(launches),
-            "roofline": roof,
+            "roofline": roofline(P, n_ops, n_flows, t_kern, peaks, ncu_summary(args.workload), info),
             "clocks": clk,
+            "parity": parity,
             "best": {"makespan_s": result[0] if result[1] >= 0 else None, "global_row": result[1]},
         }
         if ls:
             out["local_search"] = ls
-        if args.workload == "c2" and not args.no_extra:
-            out["north_star_config"] = north_star_config(P)
         if world == 1 and not args.no_cpu:
-            arrays = inst._arrays
-            out["cpu_baseline"] = cpu_baseline_python(arrays, rows, args.cpu_seconds)
-            out["cpu_baseline_native"] = cpu_baseline_native(arrays, rows, args.cpu_seconds / 3)
+            out["cpu_baseline"] = cpu_baseline_python(inst._arrays, rows, args.cpu_seconds)
+            out["cpu_baseline_native"] = cpu_baseline_native(orc, rows, args.cpu_seconds / 3)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     inst.close()
     if out is not None:
         print(json.dumps(out), flush=True)
+
+
+def roofline(P, n_ops, n_flows, t_kern, peaks, ncu, info) -> dict:
+    """Three fractions for the evaluator; `bound` = the tightest.
+
+    * tables: B_tab = 8α + 24β bytes per placement (op cost per op, payload or
+      comm entry per flow, 4 B CSR index per augmented link in each of the rank
+      and dispatch passes) against the shared-memory load bandwidth measured now
+      (L2 when the tables are off-chip);
+    * hbm: B_hbm = α + 8 bytes (row in, makespan out) against MEASURED_PEAKS.json;
+    * issue: issued warp-instructions per cycle / 4 schedulers per SM, from the ncu
+      capture of this exact source tree (null when the capture is stale)."""
+    hbm_peak, hbm_src = measured_hbm_peak()
+    b_hbm = n_ops + 8
+    b_tab = 8 * n_ops + 24 * n_flows
+    fr = {}
+    hbm_ach = P * b_hbm / t_kern / 1e9
+    fr["hbm"] = {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
+                 "algorithmic_bytes_per_placement": b_hbm, "peak_source": hbm_src}
+    onchip = bool(info.get("onchip", True)) or info.get("kernel", "").startswith("tpp")
+    if peaks:
+        pk = peaks["smem_TBps"] if onchip else peaks["l2_TBps"]
+        tab_ach = P * b_tab / t_kern / 1e12
+        fr["tables"] = {"achieved": tab_ach, "peak": pk, "unit": "TB/s", "frac": tab_ach / pk,
+                        "algorithmic_bytes_per_placement": b_tab, "level": "smem" if onchip else "l2",
+                        "peak_source": "measured now: " + peaks["source"], "peaks": peaks}
+    if ncu and ncu.get("current"):
+        ib = ncu.get("issue_slots_busy")
+        fr["issue"] = {"achieved": ncu.get("ipc_issued"), "peak": 4.0, "unit": "warp-inst/clk/SM", "frac": ib,
+                       "inst_per_placement": ncu.get("inst_per_row"), "source": ncu.get("source")}
+    bound = max(fr, key=lambda k: fr[k]["frac"] or 0.0)
+    top = fr[bound]
+    traffic = None
+    if ncu and ncu.get("current") and ncu.get("dram_bytes_per_row") is not None:
+        traffic = ncu["dram_bytes_per_row"] * P
+    return {"bound": bound, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
+            "frac": top["frac"], "traffic": traffic, "kernel_ms": t_kern * 1e3, "fractions": fr,
+            "ncu": ({k: ncu[k] for k in ("source_hash", "so_sha256", "current", "kernel", "dram_bytes_per_row",
+                                          "ipc_issued", "issue_slots_busy", "warps_per_sm", "l2_hit_rate",
+                                          "smem_wavefronts_per_row") if k in ncu} if ncu else None),
+            "source_hash": source_hash()}
 
 
 # ---- reference arm -------------------------------------------------------------------------
@@ -435,6 +527,7 @@ def run_reference(args):
     g = coarse_on_cpu(w)
     arrays = flat_arrays(g, w.cluster)
     n_ops = len(g)
+    n_flows = len(arrays[2])
     K = len(w.cluster.device_ids)
     cores = os.cpu_count() or 1
     # size one step for ~args.ref_step_s seconds of all-core work
@@ -462,14 +555,35 @@ def run_reference(args):
     value = n * args.steps / dt
     sample = (f"{n} placements per step of the {w.name} stream (GCOF {len(w.raw)} -> {n_ops} ops), pure-Python "
               f"restatement of opplace._schedule (oracle/pyref.py), {procs} processes")
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": w.name + f" (GCOF {len(w.raw)} -> {n_ops} ops, K={K})", "rows_per_step": n,
-                      "parallelism": f"{procs} host processes"},
+           "config": workload_config(w, n_ops, n_flows, K),
+           "rows_per_step": n, "parallelism": f"{procs} host processes",
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_distributed(args) -> int:
+    """`--gpus N` outside torchrun: start N ranks ourselves (same contract as the
+    driver's torchrun launch).  Refuses when the box has fewer than N GPUs."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if args.impl == "ours" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but this box has {have} GPU(s)", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -478,16 +592,22 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", default="c2", choices=("c1", "c2", "c2k8", "c3", "c4"))
+    ap.add_argument("--workload", default="c2k8", choices=WORKLOADS)
     ap.add_argument("--rows", type=int, default=1 << 20, help="placements per GPU per step")
     ap.add_argument("--tune", default="", help="G:U:ready_cap launch-shape override")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the K=8 north-star config line")
-    ap.add_argument("--local-search", action="store_true", default=True)
+    ap.add_argument("--no-local-search", dest="local_search", action="store_false")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":
+            run_reference(args)  # host CPU arm: rank 0 only, nothing to launch
+            return
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

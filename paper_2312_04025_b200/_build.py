@@ -18,6 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libmoirai_b200.so"
+PEAKS_LIB = PKG / "libmoirai_peaks.so"  # on-chip bandwidth microbenchmarks (bench.py roofline peaks)
 OBJ = PKG / "_obj"
 
 SOURCES = ["mp_eval.cu", "mp_instance.cu", "mp_bnb.cu", "mp_aux.cu", "mp_coarsen.cu", "mp_io.cpp"]
@@ -63,6 +64,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = [OBJ / (s.stem + ".o") for s in srcs]
     if force or jobs or _stale(LIB, objs):
         run([nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static", "-lrt",
+             "-lpthread", "-ldl"])
+    psrc = CSRC / "mp_peaks.cu"
+    if psrc.exists() and (force or _stale(PEAKS_LIB, [psrc])):
+        run([nvcc(), *ARCH, *NVFLAGS, "-shared", "-o", str(PEAKS_LIB), str(psrc), "-lcudart_static", "-lrt",
              "-lpthread", "-ldl"])
     return LIB
 
