@@ -35,20 +35,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_smem(int iters, unsigned long l
     const uint32_t lane_off = (tid & 31) * W;
     const uint32_t wbase = (tid >> 5) * warp_span;
     constexpr uint32_t mask = kSmemBytes - 1;
+    // ld.volatile: ptxas may neither merge nor hoist the loads (plain ld.shared
+    // inside asm volatile is still an ordinary PTX load that ptxas can CSE); the
+    // row walked by a warp advances every iteration
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const uint32_t a = base + ((wbase + (it * 8 + u) * (32 * warp_span) + lane_off) & mask);
+            const uint32_t a = base + ((wbase + (it * 8 + u) * (33 * warp_span) + lane_off) & mask);
             if constexpr (W == 16) {
                 uint32_t x, y, z, w;
-                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
+                asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
                 acc0 ^= x;
                 acc1 ^= y;
                 acc2 ^= z;
                 acc3 ^= w;
             } else {
                 uint32_t x, y;
-                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
+                asm volatile("ld.volatile.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
                 acc0 ^= x;
                 acc1 ^= y;
             }

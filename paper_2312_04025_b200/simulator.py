@@ -135,6 +135,8 @@ def check_feasibility(schedule: Schedule, gc: CompGraph, c: Cluster, mesh: Effec
     for i in ids:
         if i not in assign or assign[i] not in devs:
             raise KeyError(f"schedule does not place op {i} on a known device")
+    if n_ops == 0:
+        return []  # nothing to audit (the reference's loops are empty)
     with Instance(gc, c, mesh, _fill_missing=float("inf")) as inst:
         row = inst.encode([assign])[0]
         st = np.asarray([starts[n] for n in ids + flow_ids], dtype=np.float64)

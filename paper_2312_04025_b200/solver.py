@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .errors import CycleError, MemoryExceededError, MissingCostError, TooLargeError
+from .errors import CycleError, DeviceLimitError, MemoryExceededError, MissingCostError, TooLargeError
 from .graph import CompGraph, find_cycle, topo_order
 from .placement import Schedule, Solution, Status
 from .profiles import Cluster, EffectiveMesh, effective_bandwidth
@@ -50,12 +50,22 @@ class Instance:
     order, device index = rank of the device id.  Validation order matches the
     reference: empty graph, then missing costs (first op, then first device, in
     ascending order), then cycles.
+
+    Departures: clusters of more than 16 devices raise
+    :class:`DeviceLimitError` before anything is built; a NaN compute time raises
+    ``ValueError`` (the reference accepts NaN, ``graph.py:59-61`` checks ``t < 0``
+    only, but its dispatch order is then defined by NaN comparisons of Python
+    tuples; this package does not restate that).
     """
+
+    MAX_DEVICES = 16  # csrc/mp_common.cuh MP_MAX_DEV
 
     def __init__(self, gc: CompGraph, c: Cluster, mesh: EffectiveMesh, device: int = 0,
                  _fill_missing: float | None = None):
         if len(gc) == 0:
             raise ValueError("cannot place an empty graph")
+        if len(c.device_ids) > self.MAX_DEVICES:
+            raise DeviceLimitError(len(c.device_ids), self.MAX_DEVICES)
         self.gc, self.cluster, self.mesh = gc, c, mesh
         self.device_ids = c.device_ids
         self.dev_index = {d: k for k, d in enumerate(self.device_ids)}
@@ -76,7 +86,8 @@ class Instance:
                 cost[i, k] = t
         if np.isnan(cost).any():
             i, k = map(int, np.argwhere(np.isnan(cost))[0])
-            raise MissingCostError(self.op_ids[i], self.device_ids[k])
+            raise ValueError(f"op {self.op_ids[i]} has a NaN compute time on device {self.device_ids[k]}; "
+                             "NaN costs are not supported")
         mem = np.asarray([gc.node(i).mem_bytes for i in self.op_ids], dtype=np.int64)
         cap = np.asarray([c.device(d).mem_bytes for d in self.device_ids], dtype=np.int64)
         bw = np.zeros((K, K), dtype=np.float64)
@@ -174,6 +185,12 @@ def _as_instance(gc, c=None, mesh=None) -> tuple[Instance, bool]:
 
 def _rows(inst: Instance, placements) -> np.ndarray:
     if isinstance(placements, np.ndarray):
+        if placements.dtype != np.uint8:
+            # no wrap-around: a device index >= 256 must not alias a valid one
+            if not np.issubdtype(placements.dtype, np.integer):
+                raise ValueError("placements must hold integer device indices")
+            if placements.size and (placements.min() < 0 or placements.max() >= inst.K):
+                raise ValueError(f"device indices must lie in [0, {inst.K})")
         rows = np.ascontiguousarray(placements, dtype=np.uint8)
         if rows.ndim != 2 or rows.shape[1] != inst.n_ops:
             raise ValueError(f"placements must be uint8 [P, {inst.n_ops}]")
@@ -299,7 +316,7 @@ def brute_force(gc: CompGraph, c: Cluster, mesh: EffectiveMesh) -> Solution:
 
 
 def solve_exact(gc: CompGraph, c: Cluster, mesh: EffectiveMesh,
-                budget: SolveBudget | None = None, *, seed_chains: int = 1024,
+                budget: SolveBudget | None = None, *, seed_chains: int | None = None,
                 seed_moves: int | None = None) -> Solution:
     """Branch and bound over assignments on the GPU (``solver.py:172-254``).
 
@@ -315,12 +332,21 @@ def solve_exact(gc: CompGraph, c: Cluster, mesh: EffectiveMesh,
       ``Status.OPTIMAL`` with ``gap`` set, objective within ``1/(1-gap)`` of the optimum.
     * node / time limits stop between rounds: ``Status.FEASIBLE`` with the
       incumbent, or ``Status.BUDGET`` without one (``solver.py:246-254``).
+      ``node_limit`` counts bounded nodes and a round never starts past it; the
+      time limit is checked between rounds (a round bounds at most 65 536
+      children).
 
-    The incumbent is seeded with a GPU local search (``seed_chains`` chains from
-    seeded random rows and the two greedy baselines); at gap 0 seeds change the
-    work, never the answer.
+    By default (``seed_chains=None``) the incumbent is seeded with a GPU local
+    search of 1024 chains (from seeded random rows and the two greedy
+    baselines) when no node or time limit is set; at gap 0 seeds change the
+    work, never the answer.  With a limit no seed is used by default, so a
+    search stopped before its first leaf reports ``Status.BUDGET`` exactly where
+    the reference does; an explicit ``seed_chains > 0`` opts back in (a stopped
+    search then reports ``Status.FEASIBLE`` with the seed).
     """
     budget = budget or SolveBudget()
+    if seed_chains is None:
+        seed_chains = 0 if (budget.node_limit is not None or budget.time_limit_s is not None) else 1024
     with Instance(gc, c, mesh) as inst:
         n, k = inst.n_ops, inst.K
         order = topo_order(gc)

@@ -44,15 +44,23 @@ def _num(s: str):
         return None
 
 
+_SCALE = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9,
+          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def read_raw(rep: str, kernel: str) -> list[dict]:
+    """Raw-page metrics of every launch of `kernel`, times in ns and sizes in bytes."""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    head = rows[0]
+    head, units = rows[0], rows[1]
     out = []
-    for r in rows[2:]:  # row 1 = units
+    for r in rows[2:]:
         d = dict(zip(head, r))
         if kernel in d.get("Kernel Name", ""):
+            for h, u in zip(head, units):
+                if u in _SCALE and _num(d[h]) is not None:
+                    d[h] = str(_num(d[h]) * _SCALE[u])
             out.append(d)
     return out
 

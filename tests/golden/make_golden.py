@@ -20,6 +20,11 @@ Populations (reference test file:line they come from):
               raw graphs, overrides (test_fusion.py:313-321)
 * workloads   C1-C4 coarse graphs + 16 seeded placements each: reference makespans
 * synth       sha256 of gen_synthetic outputs for the C1/C5 specs
+* simulate    reference ``simulate`` event lists: random_instance seeds 2000-2039
+              (test_simulator.py:74-89) and 0-19 (test_simulator.py:60-71), the
+              frozen fixtures (test_simulator.py:25-57), graphs whose costs are
+              missing on devices no op is placed on (simulator.py:85-96), and the
+              validation errors (unknown device, missing placed cost, memory)
 """
 
 from __future__ import annotations
@@ -417,10 +422,73 @@ def make_synth():
     return out
 
 
+def _ser_events(events) -> list:
+    return [[H(e.time_s), e.kind.value, e.node, e.device, list(e.channel) if e.channel else None] for e in events]
+
+
+def make_simulate():
+    cases = []
+
+    def add(tag, g, c, assigns):
+        mesh = ref.effective_bandwidth(c)
+        res = []
+        for a in assigns:
+            try:
+                ms, ev = ref.simulate(g, c, mesh, a)
+                res.append({"status": "ok", "makespan": H(ms), "events": _ser_events(ev)})
+            except ref.MemoryExceededError as e:
+                res.append({"status": "memory", "device": e.device, "overflow": e.overflow})
+            except ref.MissingCostError as e:
+                res.append({"status": "missing", "op": e.op, "device": e.device})
+            except KeyError as e:
+                res.append({"status": "keyerror", "message": str(e)})
+        cases.append({"name": tag, "graph": ser_graph(g), "cluster": ser_cluster(c),
+                      "assignments": [{str(k): v for k, v in a.items()} for a in assigns], "results": res})
+
+    for trial in range(40):
+        rng = random.Random(2000 + trial)
+        g, c = rc.random_instance(rng, tight_ok=False)
+        add(f"sweep-{2000 + trial}", g, c, [{i: rng.choice(c.device_ids) for i in g.node_ids}])
+    for trial in range(20):
+        rng = random.Random(trial)
+        g, c = rc.random_instance(rng, tight_ok=False)
+        add(f"sorted-{trial}", g, c, [{i: rng.choice(c.device_ids) for i in g.node_ids}])
+    c = rc.two_device_cluster()
+    add("single_op", ref.CompGraph([ref.OpNode(1, "conv", 1, {0: 2.0, 1: 5.0})], []), c, [{1: 0}, {1: 1}])
+    g, c = rc.split_chain()
+    add("split_chain", g, c, [{1: 0, 2: 1}, {1: 1, 2: 0}, {1: 0, 2: 0}])
+    g, c = rc.two_op_chain()
+    add("two_op_chain", g, c, [{1: 0, 2: 0}, {1: 0, 2: 1}])
+    # costs present only on the devices the placement uses (simulator.py:85-96
+    # checks the placed device alone); sparse-cost copies of random instances
+    for trial in range(30):
+        rng = random.Random(5000 + trial)
+        g, c = rc.random_instance(rng, tight_ok=False)
+        assign = {i: rng.choice(c.device_ids) for i in g.node_ids}
+        nodes = []
+        for n in g.nodes:
+            keep = {assign[n.id]: n.compute_time[assign[n.id]]}
+            for d in c.device_ids:
+                if d != assign[n.id] and rng.random() < 0.4:
+                    keep[d] = n.compute_time[d]
+            nodes.append(ref.OpNode(n.id, n.op_type, n.mem_bytes, keep, n.members, n.type_seq, n.tag))
+        gs = ref.CompGraph(nodes, list(g.edges))
+        add(f"sparse-{5000 + trial}", gs, c, [assign])
+    # validation errors, in the reference's order
+    c = rc.two_device_cluster(mem=10)
+    add("memory", ref.CompGraph([ref.OpNode(1, "conv", 11, {0: 1.0, 1: 1.0})], []), c, [{1: 0}])
+    g2 = ref.CompGraph([ref.OpNode(1, "conv", 1, {0: 1.0}), ref.OpNode(2, "bn", 1, {0: 1.0, 1: 2.0})],
+                       [ref.FlowEdge(1, 2, 1000)])
+    add("missing_on_placed", g2, rc.two_device_cluster(), [{1: 1, 2: 0}, {1: 0, 2: 1}])
+    add("unknown_device", g2, rc.two_device_cluster(), [{1: 0, 2: 7}])
+    return cases
+
+
 def main():
     jobs = {"schedules.json": make_schedules, "brute_force.json": make_brute, "gcof.json": make_gcof,
             "workload_evals.json": make_workload_evals, "synth.json": make_synth,
-            "solve_exact.json": make_solve_exact, "aux.json": make_aux}
+            "solve_exact.json": make_solve_exact, "aux.json": make_aux,
+            "simulate.json": make_simulate}
     only = set(sys.argv[1:])
     for fname, fn in jobs.items():
         if only and fname not in only:

@@ -209,8 +209,30 @@ def test_mip_start_names_and_values_follow_the_reference_model():
         rg = opplace.CompGraph([opplace.OpNode(1, "conv", 10, {0: 2.0, 1: 4.0}),
                                 opplace.OpNode(2, "bn", 10, {0: 1.0, 1: 0.5})], [opplace.FlowEdge(1, 2, 10_000_000)])
         mdl = opplace.build_model(rg, rc, opplace.effective_bandwidth(rc))
-        names = {v.name for v in mdl.vars}
-        assert set(vals) <= names
+        names = [v.name for v in mdl.vars]
+        assert set(vals) == set(names)  # a complete start: every variable, T included
+        x = [vals[nm] for nm in names]
+        for row in mdl.rows:  # and a feasible one: every row of the model holds
+            lhs = sum(cf * x[v] for cf, v in row.terms)
+            assert (lhs <= row.rhs + 1e-9) if row.sense == "<=" else abs(lhs - row.rhs) <= 1e-9, row.name
+    assert vals["T"] == 4.5
+
+
+def test_mip_start_ordering_binaries_follow_the_schedule():
+    """dord / dcom exist only for unrelated pairs (milp.py:141-145) and say which
+    side runs first (ord1/ord2, milp.py:196-206)."""
+    from paper_2312_04025_b200.mipstart import mip_start_values
+
+    c = mp.Cluster([mp.Device(0, 100), mp.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
+    g = mp.CompGraph([mp.OpNode(1, "a", 1, {0: 1.0, 1: 1.0}), mp.OpNode(2, "b", 1, {0: 1.0, 1: 1.0}),
+                      mp.OpNode(3, "c", 1, {0: 1.0, 1: 1.0})],
+                     [mp.FlowEdge(1, 3, 5_000_000), mp.FlowEdge(2, 3, 5_000_000)])
+    # ops 1, 2 unrelated on device 0 (2 first), 3 on device 1; flows 4 (1->3), 5 (2->3)
+    s = mp.Schedule({1: 0, 2: 0, 3: 1}, {2: 0.0, 1: 1.0, 5: 1.0, 4: 2.0, 3: 3.0},
+                    {2: 1.0, 1: 2.0, 5: 2.0, 4: 3.0, 3: 4.0}, {4: (0, 1), 5: (0, 1)}, 4.0)
+    v = mip_start_values(s, g, c)
+    assert v["dord_1_2"] == 0.0 and "dord_1_3" not in v and "dord_2_3" not in v
+    assert v["dcom_4_5"] == 0.0 and v["T"] == 4.0
 
 
 def test_bulk_object_construction_restores_the_collector():

@@ -155,7 +155,7 @@ def test_budgeted_solve_on_coarse_graph_is_clean(oracle_mod):
     c = cluster_from(case["cluster"])
     assert (len(g.nodes), len(g.edges)) == (30, 57)
     mesh = mp.effective_bandwidth(c)
-    sol = mp.solve_exact(g, c, mesh, mp.SolveBudget(gap=0.05, time_limit_s=30.0))
+    sol = mp.solve_exact(g, c, mesh, mp.SolveBudget(gap=0.05, time_limit_s=30.0), seed_chains=1024)
     assert sol.status in (mp.Status.OPTIMAL, mp.Status.FEASIBLE)
     ms, _ = mp.simulate(g, c, mesh, sol.placement)
     assert ms == sol.objective_s
@@ -168,9 +168,9 @@ def test_budgeted_solve_on_coarse_graph_is_clean(oracle_mod):
 def test_node_and_time_limits():
     g, c = _random_instance(5, 16, 4, tight=False)
     mesh = mp.effective_bandwidth(c)
-    s1 = mp.solve_exact(g, c, mesh, mp.SolveBudget(node_limit=1), seed_chains=0)
+    s1 = mp.solve_exact(g, c, mesh, mp.SolveBudget(node_limit=1))  # no seed with a limit: the reference's BUDGET
     assert s1.status is mp.Status.BUDGET and s1.schedule is None and math.isinf(s1.objective_s)
-    s2 = mp.solve_exact(g, c, mesh, mp.SolveBudget(node_limit=1))
+    s2 = mp.solve_exact(g, c, mesh, mp.SolveBudget(node_limit=1), seed_chains=1024)  # opt-in seed
     assert s2.status is mp.Status.FEASIBLE and s2.schedule is not None and s2.gap is None
     s3 = mp.solve_exact(g, c, mesh, mp.SolveBudget(time_limit_s=0.0))
     assert s3.status in (mp.Status.FEASIBLE, mp.Status.BUDGET)

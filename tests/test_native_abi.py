@@ -73,3 +73,43 @@ def test_validation_before_the_gpu():
         mp.Instance(mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0})], []), c, mesh)
     assert (ei.value.op, ei.value.device) == (1, 1)
     assert np.isnan(np.nan)
+
+
+def test_departures_raise_clear_errors_before_the_gpu():
+    """Documented departures of the drop-in surface: more than
+    16 devices -> DeviceLimitError; a NaN cost -> ValueError (not MissingCostError,
+    which the reference reserves for absent entries)."""
+    devs = [mp.Device(k, 10) for k in range(17)]
+    c17 = mp.Cluster(devs, {(a, b): 1e6 for a in range(17) for b in range(17) if a != b})
+    g = mp.CompGraph([mp.OpNode(1, "conv", 1, {k: 1.0 for k in range(17)})], [])
+    with pytest.raises(mp.DeviceLimitError) as ei:
+        mp.Instance(g, c17, mp.effective_bandwidth(c17))
+    assert (ei.value.devices, ei.value.limit) == (17, 16)
+    assert isinstance(ei.value, mp.NativeError)
+    c = mp.Cluster([mp.Device(0, 10), mp.Device(1, 10)], {(0, 1): 1e6, (1, 0): 1e6})
+    with pytest.raises(ValueError, match="NaN"):
+        mp.Instance(mp.CompGraph([mp.OpNode(1, "conv", 1, {0: float("nan"), 1: 1.0})], []), c,
+                    mp.effective_bandwidth(c))
+
+
+def test_check_feasibility_of_an_empty_graph_is_empty():
+    """The reference's audit loops are empty for an empty graph (simulator.py:179-264)."""
+    c = mp.Cluster([mp.Device(0, 10), mp.Device(1, 10)], {(0, 1): 1e6, (1, 0): 1e6})
+    s = mp.Schedule({}, {}, {}, {}, 0.0)
+    assert mp.check_feasibility(s, mp.CompGraph([], []), c, mp.effective_bandwidth(c)) == []
+
+
+def test_non_uint8_rows_are_range_checked():
+    """int rows are not cast modulo 256 onto valid device indices."""
+    from paper_2312_04025_b200.solver import _rows
+
+    class _Inst:
+        n_ops, K = 3, 4
+
+    with pytest.raises(ValueError):
+        _rows(_Inst(), np.array([[0, 1, 260]], dtype=np.int64))
+    with pytest.raises(ValueError):
+        _rows(_Inst(), np.array([[0, -1, 2]], dtype=np.int32))
+    with pytest.raises(ValueError):
+        _rows(_Inst(), np.array([[0.0, 1.0, 2.0]]))
+    assert _rows(_Inst(), np.array([[0, 1, 3]], dtype=np.int64)).dtype == np.uint8
