@@ -45,9 +45,9 @@ int main(void) {
         mp_instance_destroy(inst);
         return 1;
     }
-    for (int p = 0; p < 8; ++p) printf("placement %d%d%d  makespan %.6f  status %d\n", rows[p * 3], rows[p * 3 + 1],
+    for (int p = 0; p < 8; ++p) printf("placement %d%d%d  makespan %a  status %d\n", rows[p * 3], rows[p * 3 + 1],
                                        rows[p * 3 + 2], ms[p], st[p]);
-    printf("best row %lld makespan %.6f\n", (long long)best, best_ms);
+    printf("best row %lld makespan %a\n", (long long)best, best_ms);
     mp_instance_destroy(inst);
     return 0;
 }

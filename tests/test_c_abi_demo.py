@@ -41,11 +41,15 @@ def test_c_demo_on_gpu_matches_python(tmp_path):
     import paper_2312_04025_b200 as mp
 
     out = subprocess.run([str(_build(tmp_path))], capture_output=True, text=True, check=True).stdout
-    got = {line.split()[1]: float(line.split()[3]) for line in out.splitlines() if line.startswith("placement")}
+    # makespans are printed with %a (exact hexadecimal): compared bit for bit
+    got = {line.split()[1]: float.fromhex(line.split()[3]) for line in out.splitlines()
+           if line.startswith("placement")}
     c = mp.Cluster([mp.Device(0, 100), mp.Device(1, 100)], {(0, 1): 5e6, (1, 0): 5e6})
     g = mp.CompGraph([mp.OpNode(1, "a", 10, {0: 2.0, 1: 4.0}), mp.OpNode(2, "b", 10, {0: 1.0, 1: 0.5}),
                       mp.OpNode(3, "c", 10, {0: 3.0, 1: 1.0})],
                      [mp.FlowEdge(1, 2, 10_000_000), mp.FlowEdge(2, 3, 20_000_000)])
     rows = np.array([[int(ch) for ch in k] for k in got], dtype=np.uint8)
     ms = mp.evaluate_batch(g, rows, c, mp.effective_bandwidth(c))
-    assert [round(x, 6) for x in ms] == [round(got[k], 6) for k in got]
+    assert [x.hex() for x in ms] == [got[k].hex() for k in got]
+    best = next(line for line in out.splitlines() if line.startswith("best row"))
+    assert float.fromhex(best.split()[4]) == min(ms)
