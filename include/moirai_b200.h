@@ -131,6 +131,7 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
 #define MP_TUNE_TPP_REG 4   /* thread-per-placement with the ready set in registers (when the
                                calibrated peak fits a 4/8/16 template) instead of shared memory */
 #define MP_TUNE_OFFCHIP 8   /* group kernel with per-placement state in global memory */
+#define MP_TUNE_TPP_ROUND1 16 /* thread-per-placement: the round-1 shared-memory-ready-set evaluator (A/B only) */
 #define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernels (used only with
                                automatic G/U) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,

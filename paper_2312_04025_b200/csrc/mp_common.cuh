@@ -104,6 +104,7 @@ struct EvalArgs {
     // have landed; null = all rows resident.  stream_fail is raised on a wait timeout.
     const unsigned int *rows_ready;
     unsigned int *stream_fail;
+    int tpp_alt;                  // 1: the round-1 shared-memory-ready-set evaluator (tpps_eval), for A/B
 };
 
 // Wait (lane 0 of a warp) until rows [.., need) of a streamed batch have landed.

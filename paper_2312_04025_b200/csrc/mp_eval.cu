@@ -806,7 +806,8 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.fast = a.fastdiv;
     v.RZ = static_cast<uint32_t>(3 * a.K);
     v.WS = v.RZ + 1;
-    const size_t rdy = static_cast<size_t>(a.rcap) * v.T;
+    // an even number of ready slots per lane (tpp2_eval scans two per iteration)
+    const size_t rdy = static_cast<size_t>((a.rcap + 1) & ~1) * v.T;
     v.rE = reinterpret_cast<unsigned long long *>(v.clk + static_cast<size_t>(3 * a.K + 2) * v.T);
     v.rR = v.rE + rdy;
     v.rM = v.rR + rdy;
@@ -1393,6 +1394,295 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
     return r;
 }
 
+// ---- thread per placement, lean evaluator (round 2) -------------------------------------
+// Same semantics, tables and shared-memory layout as tpps_eval; restructured for
+// fewer issued instructions per dispatch step (ncu: the round-1 evaluator spent
+// ~880 warp-instructions per step, 24 % in the ready scan, 50 % on successors):
+//   * ready slots past a lane's count hold a NaN est: max() keeps NaN and every
+//     ordered compare with NaN is false, so a stale slot can never win and the
+//     scan needs no `s < nr` masking; it runs two slots per iteration over an
+//     even slot count;
+//   * keys compare as fp64 (DSETP: one instruction per relation); all times are
+//     >= +0.0 and never NaN for a live entry;
+//   * the scan tracks only (e, rank, id, slot); the winner's meta word is read
+//     once after the loop;
+//   * per-lane global state is addressed from a per-lane base with 32-bit
+//     offsets (IMAD.WIDE.U32), and the multi-input tie id and npred share one
+//     64-bit word, so a consumer update is one 8-byte and one 16-byte round trip.
+// Global per-lane state (lane-interleaved [index][L], tpp_state_bytes): rank f64
+// [n_ops], est f64 [n_multi], tie | npred << 32 u64 [n_multi].
+template <bool COLO>
+__device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs &a, bool live, bool bad, int cap) {
+    const int T = v.T, n_ops = v.n_ops, K = v.K;
+    const unsigned char *__restrict__ rowl = v.rowt + v.tid;  // op x: rowl[(x >> 1) * T], nibble (x & 1)
+    double *__restrict__ clk = v.clk + v.tid;                   // clock slot s: clk[s * T]
+    unsigned long long *__restrict__ ld = v.ld + v.tid;
+    const unsigned L8 = static_cast<unsigned>(v.L) * 8u;
+    const long long gl = static_cast<long long>(blockIdx.x) * T + v.tid;
+    unsigned char *g0 = a.gstate + gl * 8;
+    unsigned char *__restrict__ g_rank = g0;
+    unsigned char *__restrict__ g_mest = g0 + static_cast<long long>(n_ops) * v.L * 8;
+    unsigned char *__restrict__ g_mtn = g0 + static_cast<long long>(n_ops + a.n_multi) * v.L * 8;
+    auto grank = [&](int j) -> double * {
+        return reinterpret_cast<double *>(g_rank + static_cast<unsigned long long>(static_cast<unsigned>(j) * L8));
+    };
+    auto gmest = [&](unsigned k) -> double * {
+        return reinterpret_cast<double *>(g_mest + static_cast<unsigned long long>(k * L8));
+    };
+    auto gmtn = [&](unsigned k) -> unsigned long long * {
+        return reinterpret_cast<unsigned long long *>(g_mtn + static_cast<unsigned long long>(k * L8));
+    };
+    const double *__restrict__ T_cost = v.T_cost;
+    const long long *__restrict__ T_mem = v.T_mem;
+    const long long *__restrict__ T_cap = v.T_cap;
+    const double *__restrict__ T_bw = v.T_bw;
+    const double *__restrict__ T_rbw = v.T_rbw;
+    const double2 *__restrict__ T_rec = v.T_rec;
+    const uint32_t *__restrict__ T_out_beg = v.T_out_beg;
+    const uint32_t *__restrict__ T_fdst = v.T_fdst;
+    const uint32_t *__restrict__ T_mi = v.T_mi;
+    const uint32_t *__restrict__ T_lvl = v.T_lvl;
+    const uint32_t *__restrict__ T_srcs = v.T_srcs;
+    const uint32_t *__restrict__ T_mdeg = v.T_mdeg;
+    const uint32_t *__restrict__ T_mop = v.T_mop;
+    const double *__restrict__ T_fpay = v.T_fpay;
+    const int fast = v.fast;
+    const uint32_t RZ = v.RZ, WS = v.WS;
+    const int capA = (a.rcap + 1) & ~1;
+    unsigned long long *__restrict__ rE = v.rE + v.tid;  // slot s: rE[s * T]; rank / meta at fixed offsets
+    const size_t DR = static_cast<size_t>(v.rR - v.rE), DM = static_cast<size_t>(v.rM - v.rE);
+    auto dev = [&](int x) -> int { return (rowl[(x >> 1) * T] >> ((x & 1) << 2)) & 15; };
+    TppResult r;
+    // ---- 1. memory feasibility (solver.py:82-87) ------------------------------------
+    int status = bad ? MP_ROW_BAD_DEVICE : MP_ROW_OK;
+    int over_dev = -1;
+    long long over_by = 0;
+    for (int k = 0; k < K; ++k) ld[k * T] = 0ULL;
+    if (live && !bad) {
+        for (int i = 0; i < n_ops; ++i) ld[dev(i) * T] += static_cast<unsigned long long>(T_mem[i]);
+        for (int k = 0; k < K; ++k) {
+            const long long l = static_cast<long long>(ld[k * T]);
+            if (l > T_cap[k]) {
+                status = MP_ROW_MEMORY;
+                over_dev = k;
+                over_by = l - T_cap[k];
+                break;
+            }
+        }
+    }
+    const bool alive = live && status == MP_ROW_OK;
+    r.alive = alive;
+
+    // ---- 2+3. durations + rank, ops in ascending height (solver.py:89-107) -----------
+    for (int t = 0; t < n_ops; ++t) {
+        const int i = static_cast<int>(T_lvl[t]);
+        const int d = dev(i);
+        double best = 0.0;
+        const int qe = static_cast<int>(T_out_beg[i + 1]);
+        for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
+            const double2 rec = T_rec[q];
+            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+            const int dj = dev(j);
+            const double rj = *grank(j);
+            double fr = rj;
+            if (dj != d) {  // warp-divergent only in timing: both sides are short
+                const int bi = d * K + dj;
+                fr = div_bw(rec.y, T_bw[bi], T_rbw[bi], fast) + rj;
+            }
+            best = fr > best ? fr : best;
+        }
+        *grank(i) = T_cost[i * K + d] + best;
+    }
+
+    // ---- 4. dispatch state (solver.py:109-116) -----------------------------------------
+    for (int k = 0; k < a.n_multi; ++k) {
+        *gmtn(k) = static_cast<unsigned long long>(T_mop[k]) | (static_cast<unsigned long long>(T_mdeg[k]) << 32);
+        *gmest(k) = 0.0;
+    }
+    for (int k = 0; k <= static_cast<int>(WS); ++k) clk[k * T] = 0.0;
+    const unsigned long long NAN_BITS = 0xfff8000000000000ULL;
+    const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (RZ << 20) | (RZ << 26));
+    for (int s = 0; s < capA; ++s) {
+        rE[s * T] = NAN_BITS;
+        rE[DM + s * T] = SENT_M;
+    }
+    int nr = 0;
+    bool ovf = false;
+    auto insert = [&](bool ins, unsigned long long est, unsigned long long rk, uint32_t meta, uint32_t tie) {
+        // bitwise logic throughout the dispatch loop: short-circuit forms compile
+        // to branches (BSSY/BSYNC) that measured 6-15 % slower
+        const bool room = nr < cap;
+        ovf = ovf | (ins & !room);
+        if (ins & room) {
+            unsigned long long *p = rE + nr * T;
+            p[0] = est;
+            p[DR] = rk;
+            p[DM] = static_cast<unsigned long long>(meta) | (static_cast<unsigned long long>(tie) << 32);
+        }
+        nr += (ins & room) ? 1 : 0;
+    };
+    if (alive) {
+        for (int t = 0; t < a.n_src; ++t) {
+            const int i = static_cast<int>(T_srcs[t]);
+            insert(true, 0ULL, dbits(*grank(i)),
+                   static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev(i)) << 20) | (RZ << 26),
+                   static_cast<uint32_t>(i));
+        }
+    }
+    bool done = !alive || ovf;
+    double ms = 0.0;
+    while (__any_sync(kFull, !done)) {
+        const int hbw = (__reduce_max_sync(kFull, done ? 0 : nr) + 1) & ~1;
+        // -- scan the ready slots for the minimum (e, -rank, id) key -------------------
+        // (one compare-select chain; a two-chain even/odd split measured 1-2 % slower)
+        double be = kInf, br = -1.0;
+        uint32_t bi = 0xffffffffu;
+        int bs = 0;
+        const unsigned long long *p = rE;
+        for (int s = 0; s < hbw; s += 2, p += 2 * T) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const unsigned long long *q = p + u * T;
+                const double es = bitsd(q[0]);
+                const double rs = bitsd(q[DR]);
+                const unsigned long long mt = q[DM];
+                const uint32_t m = static_cast<uint32_t>(mt);
+                const double c1 = clk[((m >> 20) & 63u) * T];
+                const double c2 = clk[(m >> 26) * T];
+                double e = c1 > es ? c1 : es;  // NaN es stays NaN: never taken
+                e = c2 > e ? c2 : e;
+                const uint32_t id = (COLO & (e == es)) ? static_cast<uint32_t>(mt >> 32) : (m & MP_NODE_MASK);
+                const bool take = (e < be) | ((e == be) & ((rs > br) | ((rs == br) & (id < bi))));
+                be = take ? e : be;
+                br = take ? rs : br;
+                bi = take ? id : bi;
+                bs = take ? s + u : bs;
+            }
+        }
+        const uint32_t bm = static_cast<uint32_t>(rE[DM + bs * T]);
+        const int node = static_cast<int>(bm & MP_NODE_MASK);
+        const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+        // a finished lane may have read a vacated slot (any node id): treat it as an
+        // op with no successors so every table index below stays in range
+        const bool isop = done | (node < n_ops);
+        const int d = static_cast<int>(r1);
+        const int nodec = done ? 0 : node;
+        const int ob = static_cast<int>(T_out_beg[isop ? nodec : 0]);
+        const int cnt = done ? 0 : (isop ? static_cast<int>(T_out_beg[nodec + 1]) - ob : 1);
+        const uint32_t jflow = T_fdst[isop ? 0 : nodec - n_ops];
+        const int maxc = __reduce_max_sync(kFull, cnt);
+        // successors' loads are issued before the duration, removal and commit
+        // (none of which writes what they read)
+        constexpr int SU = 2;
+        int j_[SU], dj_[SU];
+        uint32_t pid_[SU], k_[SU];
+        unsigned long long tn_[SU];
+        double rj_[SU], cur_[SU], pay_[SU];
+        bool act_[SU];
+        auto phase_a = [&](int t0) {
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                const int t = t0 + u;
+                const bool act = t < cnt;
+                const double2 rec = T_rec[(act & isop) ? ob + t : 0];
+                const unsigned long long rb = dbits(rec.x);
+                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                j_[u] = j;
+                dj_[u] = dev(j);
+                pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
+                pay_[u] = rec.y;
+                act_[u] = act;
+                rj_[u] = *grank(j);
+                const uint32_t k = T_mi[j];
+                k_[u] = k;
+                const bool op_upd = act & !(isop & !(COLO & (dj_[u] == d)));
+                tn_[u] = 1ULL << 32;
+                cur_[u] = 0.0;
+                if (op_upd & (k != MP_NONE)) {
+                    tn_[u] = *gmtn(k);
+                    cur_[u] = *gmest(k);
+                }
+            }
+        };
+        if (maxc > 0) phase_a(0);
+        // the winner's duration: op cost, payload / bw for a crossing flow, 0 for a
+        // co-located flow dispatched as a node (colo off)
+        double bd = 0.0;
+        if (!done && node < n_ops) {
+            bd = T_cost[node * K + d];
+        } else if (!done && r1 != RZ) {
+            const int bi2 = (d - K) * K + (static_cast<int>(r2) - 2 * K);
+            bd = div_bw(T_fpay[node - n_ops], T_bw[bi2], T_rbw[bi2], fast);
+        }
+        // unordered removal: the last entry moves into the hole, the vacated slot
+        // becomes NaN (never taken)
+        const int last = nr - 1;
+        if (!done) {
+            if (bs != last) {
+                unsigned long long *h = rE + bs * T;
+                const unsigned long long *l = rE + last * T;
+                h[0] = l[0];
+                h[DR] = l[DR];
+                h[DM] = l[DM];
+            }
+            rE[last * T] = NAN_BITS;
+        }
+        nr = done ? nr : last;
+        // -- commit (solver.py:130-138) ------------------------------------------------
+        const double end = be + bd;
+        if (!done) {
+            clk[(r1 == RZ ? WS : r1) * T] = end;
+            clk[(r2 == RZ ? WS : r2) * T] = end;
+        }
+        ms = (!done & (node < n_ops) & (end > ms)) ? end : ms;
+        // -- successors (solver.py:140-145): op -> its out-flows, flow -> its consumer
+        for (int t0 = 0; t0 < maxc; t0 += SU) {
+            if (t0 > 0) phase_a(t0);
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                if (t0 + u >= maxc) break;
+                const int j = j_[u], dj = dj_[u];
+                const uint32_t pid = pid_[u];
+                const bool act = act_[u];
+                const bool multi = k_[u] != MP_NONE;
+                const bool cross = dj != d;
+                const bool via_colo = COLO & isop & !cross;
+                const bool flow_ins = act & isop & !via_colo;  // a flow enters the ready set
+                const bool op_upd = act & !flow_ins;           // j's npred / est / gate change
+                const int bi2 = cross ? d * K + dj : 0;         // computed unconditionally, selected
+                const double fdur = (isop & cross) ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                const double rj = rj_[u];
+                const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
+                                                       (static_cast<uint32_t>(2 * K + dj) << 26))
+                                                    : ((RZ << 20) | (RZ << 26)));
+                // multi-input ops keep npred / est / gate id
+                const double cur = cur_[u];
+                const uint32_t ct = static_cast<uint32_t>(tn_[u]);
+                const uint32_t np = static_cast<uint32_t>(tn_[u] >> 32) - 1u;
+                const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
+                const bool up = end > cur;
+                const double ej = multi ? (up ? end : cur) : end;
+                const uint32_t tie_new = up ? tj : ((via_colo & (end == cur) & (pid > ct)) ? pid : ct);
+                if (op_upd & multi) {
+                    *gmtn(k_[u]) = static_cast<unsigned long long>(tie_new) | (static_cast<unsigned long long>(np) << 32);
+                    *gmest(k_[u]) = ej;
+                }
+                const bool op_ins = op_upd & (!multi | (np == 0u));
+                insert(flow_ins | op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
+                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                       flow_ins ? pid : (multi ? tie_new : tj));
+            }
+        }
+        done = done | ovf | (nr == 0);
+    }
+    r.ms = ms;
+    r.status = status;
+    r.over_dev = over_dev;
+    r.over_by = over_by;
+    r.ovf = ovf;
+    return r;
+}
+
 template <int RC, bool COLO>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1490,7 +1780,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_ls_kernel(const 
 }
 
 // ---- thread per placement, ready set in shared memory ----------------------------------
-template <bool COLO>
+template <bool COLO, int VAR>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
@@ -1516,7 +1806,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
         const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
         const long long grow = a.row_base + lrow;
         const bool bad = tpp_load_row<true>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
-        const TppResult r = tpps_eval<COLO>(v, a, live, bad, a.rcap);
+        const TppResult r = VAR == 1 ? tpps_eval<COLO>(v, a, live, bad, a.rcap) : tpp2_eval<COLO>(v, a, live, bad, a.rcap);
         if (live) {
             const long long o = grow - a.out_base;
             if (r.ovf) {
@@ -1543,7 +1833,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
 // K5 on the thread-per-placement layout (shared-memory ready set): one lane per chain, the chain's row in
 // its tile column.  Same proposals, acceptance rule and ready capacity (`a.rcap`,
 // the group kernel's) as mp_ls_kernel, so results do not depend on the kernel.
-template <bool COLO>
+template <bool COLO, int VAR>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                          const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1562,7 +1852,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
         const long long srow = live ? static_cast<long long>(gc % static_cast<unsigned long long>(ls.n_seed)) : 0;
         tpp_load_row<true>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
-        const TppResult r0 = tpps_eval<COLO>(v, a, live, false, a.rcap);
+        const TppResult r0 = VAR == 1 ? tpps_eval<COLO>(v, a, live, false, a.rcap) : tpp2_eval<COLO>(v, a, live, false, a.rcap);
         double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
@@ -1572,7 +1862,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
             const int old = (*cell >> sh) & 15;
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
             if (live) *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (nd << sh));
-            const TppResult r = tpps_eval<COLO>(v, a, live, false, a.rcap);
+            const TppResult r = VAR == 1 ? tpps_eval<COLO>(v, a, live, false, a.rcap) : tpp2_eval<COLO>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
                 cur_ms = ms;
@@ -1788,14 +2078,16 @@ cudaError_t mp_launch_tpp_ls(int rc, int threads, int ctas, int smem, const Eval
 cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        for (EvalFn f : {mp_tpps_kernel<true>, mp_tpps_kernel<false>}) {
+        for (EvalFn f : {mp_tpps_kernel<true, 0>, mp_tpps_kernel<false, 0>, mp_tpps_kernel<true, 1>,
+                         mp_tpps_kernel<false, 1>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
-    EvalFn f = a.colo ? mp_tpps_kernel<true> : mp_tpps_kernel<false>;
+    EvalFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_kernel<true, 1> : mp_tpps_kernel<false, 1>)
+                              : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
@@ -1804,14 +2096,16 @@ cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, c
 cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        for (LsFn f : {mp_tpps_ls_kernel<true>, mp_tpps_ls_kernel<false>}) {
+        for (LsFn f : {mp_tpps_ls_kernel<true, 0>, mp_tpps_ls_kernel<false, 0>, mp_tpps_ls_kernel<true, 1>,
+                       mp_tpps_ls_kernel<false, 1>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
-    LsFn f = a.colo ? mp_tpps_ls_kernel<true> : mp_tpps_ls_kernel<false>;
+    LsFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_ls_kernel<true, 1> : mp_tpps_ls_kernel<false, 1>)
+                            : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();

@@ -346,6 +346,7 @@ struct mp_instance {
     // thread-per-placement variant (mp_tpp_kernel); tpp_rc == 0: not used
     bool tpp_allowed = true;
     bool tpp_reg_pref = false;   // MP_TUNE_TPP_REG
+    bool tpp_round1 = false;     // MP_TUNE_TPP_ROUND1
     bool force_offchip = false;  // MP_TUNE_OFFCHIP
     int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
@@ -491,7 +492,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         // shared-memory ready set: 24 B per entry per lane, capacity = the peak (>= 4),
         // row tile nibble-packed
         const int cap_s = ready_cap_req > 0 ? rcap : std::min(I->ready_bound, std::max(4, want));
-        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * cap_s;
+        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1);
         const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / lane_s) / 32 * 32));
         // register ready set: the smallest template >= the peak
         const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
@@ -505,7 +506,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
             I->tpp_rc = cap_s;
             I->tpp_threads = Ts;
             I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
-                                           (8LL * (3 * K + 2) + 24LL * cap_s) * Ts);
+                                           (8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1)) * Ts);
         } else if (rc > 0 && Tr >= 128) {
             I->tpp_kind = 1;
             I->tpp_rc = rc;
@@ -523,7 +524,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
 void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
     const long long avail = static_cast<long long>(MP_SMEM_DYN_MAX) - I->to.bytes - 32;
     const long long row = (I->n_ops + 1) / 2;  // nibble-packed row tile
-    const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * cap;
+    const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * ((cap + 1) & ~1);  // even slot count
     const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
     *threads = T >= 64 ? T : 0;
     *smem = static_cast<int>(I->to.bytes + ((row * T + 15) & ~15LL) + (per_lane - row) * T);
@@ -555,6 +556,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.n_multi = I->n_multi;
     a.colo = I->colo ? 1 : 0;
     a.fastdiv = I->fastdiv ? 1 : 0;
+    a.tpp_alt = I->tpp_round1 ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
     a.lanes_used = wide ? I->wide.U : I->main.U;
@@ -928,6 +930,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->colo = I->colo_ok && !(flags & MP_TUNE_NO_COLO);
     I->tpp_allowed = !(flags & MP_TUNE_NO_TPP);
     I->tpp_reg_pref = (flags & MP_TUNE_TPP_REG) != 0;
+    I->tpp_round1 = (flags & MP_TUNE_TPP_ROUND1) != 0;
     I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--no-tpp", action="store_true")
     ap.add_argument("--tpp-reg", action="store_true")
     ap.add_argument("--offchip", action="store_true")
+    ap.add_argument("--round1", action="store_true", help="the round-1 TPP evaluator (A/B)")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     args = ap.parse_args()
@@ -53,7 +54,7 @@ def main():
     for spec in args.G.split(","):
         G, U = (int(x) for x in (spec.split(":") + ["0"])[:2])
         inst.tune(G, args.ctas_per_sm, ready_cap=args.rcap, colo=not args.no_colo, lanes_used=U, tpp=not args.no_tpp,
-                  tpp_registers=args.tpp_reg, offchip=args.offchip)
+                  tpp_registers=args.tpp_reg, offchip=args.offchip, tpp_round1=args.round1)
         info = inst.info()
         best = C.c_int64()
         bms = C.c_double()

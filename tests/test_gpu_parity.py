@@ -235,7 +235,7 @@ SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (1, 2, 4, 8, 16,
 # fits its register capacity (4 / 8 / 16 entries; ready_cap=3 forces reruns)
 TPP_SHAPES = [dict(), dict(colo=False), dict(ready_cap=3), dict(ready_cap=6, colo=False), dict(ready_cap=12),
               dict(tpp_registers=True), dict(tpp_registers=True, colo=False), dict(tpp_registers=True, ready_cap=3),
-              dict(tpp_registers=True, ready_cap=12)]
+              dict(tpp_registers=True, ready_cap=12), dict(tpp_round1=True), dict(tpp_round1=True, ready_cap=3)]
 
 
 @pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
@@ -274,7 +274,7 @@ def test_eval_vs_oracle_workloads(oracle_mod, name):
         rows = workloads.placements(w.seed, 4096 if name != "c5" else 256, inst.n_ops, inst.K)
         want, wst = orc.eval_batch(rows, threads=8)
         for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False),
-                      dict(ready_cap=3), dict(tpp=False), dict(tpp_registers=True)):
+                      dict(ready_cap=3), dict(tpp=False), dict(tpp_registers=True), dict(tpp_round1=True)):
             inst.tune(**shape)
             ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
             assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)
