@@ -189,11 +189,12 @@ __device__ __forceinline__ double bitsd(unsigned long long b) {
 }
 
 // payload / bw, bit-identical to IEEE division: q0 = a*y, r = a - b*q0 (exact
-// with an fma), q = q0 + r*y (Markstein).  Used only when the instance verified
-// it against IEEE division for every (payload, bandwidth) pair it can produce
-// (mp_instance.cu k_verify_div); otherwise the IEEE division routine runs.
+// with an fma), q = q0 + r*y (Markstein).  Used only for device pairs whose
+// reciprocal the instance verified against IEEE division for every payload it
+// can produce (mp_instance.cu k_verify_div); a pair that failed has y = -1 in
+// the table and takes the IEEE division routine.
 __device__ __forceinline__ double div_bw(double a, double b, double y, int fast) {
-    if (fast) {
+    if (fast & (y > 0.0)) {
         const double q0 = __dmul_rn(a, y);
         const double r = __fma_rn(-q0, b, a);
         return __fma_rn(r, y, q0);

@@ -133,11 +133,13 @@ __global__ void k_slots(int n_ops, int n_flows, const unsigned int *sorted_f, co
 
 // Markstein division check: for every flow payload and ordered device pair the
 // instance can produce, q0 = a*y, q = fma(fma(-q0, b, a), y, q0) must equal the
-// IEEE quotient bit for bit; any mismatch disables the fast path.
-__global__ void k_verify_div(int n_flows, int K, const double *pay_d, const unsigned char *blob, TabOff to,
+// IEEE quotient bit for bit; a mismatch disables the fast path for THAT pair
+// (its reciprocal becomes -1, div_bw then divides).  Concurrent readers of a
+// pair being disabled see either value; both paths give the IEEE quotient.
+__global__ void k_verify_div(int n_flows, int K, const double *pay_d, unsigned char *blob, TabOff to,
                              unsigned int *mismatch) {
     const double *bw = reinterpret_cast<const double *>(blob + to.bw);
-    const double *rbw = reinterpret_cast<const double *>(blob + to.rbw);
+    double *rbw = reinterpret_cast<double *>(blob + to.rbw);
     const long long total = static_cast<long long>(n_flows) * K * K;
     for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
          x += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -145,9 +147,14 @@ __global__ void k_verify_div(int n_flows, int K, const double *pay_d, const unsi
         const int p = static_cast<int>(x % (K * K));
         if (p / K == p % K) continue;
         const double a = pay_d[f], b = bw[p];
-        const double fast = div_bw(a, b, rbw[p], 1);
+        const double y = rbw[p];
+        const double q0 = __dmul_rn(a, y);
+        const double fast = __fma_rn(__fma_rn(-q0, b, a), y, q0);
         const double slow = a / b;
-        if (__double_as_longlong(fast) != __double_as_longlong(slow)) atomicOr(mismatch, 1u);
+        if (y > 0.0 && __double_as_longlong(fast) != __double_as_longlong(slow)) {
+            rbw[p] = -1.0;
+            atomicAdd(mismatch, 1u);
+        }
     }
 }
 
@@ -328,6 +335,7 @@ struct mp_instance {
     bool colo_ok = false;  // every op cost and crossing-flow duration > 0
     bool colo = false;     // co-located flows skipped
     bool fastdiv = false;  // Markstein division verified for this instance
+    int slow_div_pairs = 0;
     int sms = 0;
     int rcap_target = 32;
     int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
@@ -800,7 +808,8 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     MP_CUDA_I(cudaMemcpyAsync(h_nsel, nsel, sizeof(h_nsel), cudaMemcpyDeviceToHost, I->stream));
     MP_CUDA_I(cudaStreamSynchronize(I->stream));
     I->n_src = h_nsel[0];
-    I->fastdiv = h_nsel[2] == 0;
+    I->fastdiv = true;                 // per pair: failing pairs were disabled in the table
+    I->slow_div_pairs = h_nsel[2];     // (payload, pair) mismatches found (0 = every pair fast)
     I->n_sinks = static_cast<int>(be.n_sinks);
     I->ready_bound = std::min(I->n_nodes, n_flows - n_ops + I->n_src + I->n_sinks);
     // Skipping co-located flows is exact when every op cost and every crossing
