@@ -296,6 +296,8 @@ typedef struct mp_coarsen_output {
     int32_t *out_src;           /* [n_edges] group index                             */
     int32_t *out_dst;
     int64_t *out_payload;
+    int32_t ordered_replay;     /* 1: order hazards present, the DFS was replayed in order;
+                                   0: candidate chains resolved in parallel */
 } mp_coarsen_output;
 
 int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device,

@@ -107,7 +107,7 @@ class mp_coarsen_output(C.Structure):
         ("mem_beg", C.POINTER(C.c_int32)), ("members", C.POINTER(C.c_int32)),
         ("grp_mem", C.POINTER(C.c_int64)), ("grp_cost", C.POINTER(C.c_double)),
         ("out_src", C.POINTER(C.c_int32)), ("out_dst", C.POINTER(C.c_int32)),
-        ("out_payload", C.POINTER(C.c_int64)),
+        ("out_payload", C.POINTER(C.c_int64)), ("ordered_replay", C.c_int32),
     ]
 
 

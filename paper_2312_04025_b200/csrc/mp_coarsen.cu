@@ -168,17 +168,27 @@ __global__ void k_split_keys(int E, const unsigned long long *keys, int *dst, in
     }
 }
 
-__global__ void k_make_keys(int E, const int *src, const int *dst, unsigned long long *keys, int *indeg) {
+// also flags an edge that does not go from a lower to a higher node index: when
+// every edge ascends, the index order is a topological order and the graph is a
+// DAG without running Kahn (validate_dag, graph.py:267-300, then has nothing to find)
+__global__ void k_make_keys(int E, const int *src, const int *dst, unsigned long long *keys, int *indeg,
+                            int *descending) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
         keys[e] = (static_cast<unsigned long long>(static_cast<unsigned>(src[e])) << 32) |
                   static_cast<unsigned>(dst[e]);
         atomicAdd(&indeg[dst[e]], 1);
+        if (src[e] >= dst[e]) atomicExch(descending, 1);
     }
 }
 
 // Kahn from the sources (graph.py:274-288); *seen < V means a cycle.
 __global__ void __launch_bounds__(1024) k_kahn(int V, const int *obeg, const int *odst, int *deg, int *fa, int *fb,
-                                               int *seen) {
+                                               int *seen, const int *run_if_clean, const int *descending) {
+    if (run_if_clean && *run_if_clean != 0) return;  // hazards: the shared-memory DFS kernel runs Kahn
+    if (*descending == 0) {  // every edge ascends: acyclic (the level-synchronous pass costs ~0.5 us per level)
+        if (threadIdx.x == 0) *seen = V;
+        return;
+    }
     __shared__ int s_cur, s_next;
     if (threadIdx.x == 0) s_cur = 0;
     __syncthreads();
@@ -206,6 +216,107 @@ __global__ void __launch_bounds__(1024) k_kahn(int V, const int *obeg, const int
         __syncthreads();
     }
     if (threadIdx.x == 0) *seen = total;
+}
+
+// ---- K1p: order-independent graphs, resolved in parallel ---------------------------------
+// A *candidate* edge t -> w is one the reference could ever fuse: t has a single
+// successor w and seq(t) + seq(w) occurs contiguously in some rule pattern (a
+// merge of cur (tail t) with nxt (head w) needs seq(cur) + seq(nxt) to be a rule
+// prefix, which contains seq(t) + seq(w) contiguously).  The graph is
+// ORDER-HAZARD-FREE when every candidate edge enters a node of in-degree 1 and no
+// node has parallel edges.  Then:
+//   * a node with in-degree >= 2 has no candidate in-edge, so it is never absorbed:
+//     every merge joins a group whose tail is t to the singleton {w} along a
+//     candidate edge (an absorbed non-head member would need a second, candidate
+//     in-edge), and no transitive collapse can occur (all successors of a
+//     multi-output t in one group would again need such a member);
+//   * w's only predecessor is t, so the DFS reaches w only from t's group, at the
+//     moment t is that group's tail: the decision "merge w" depends only on the
+//     group's sequence, i.e. on the walk along the candidate chain from its first
+//     node, which is always a head (it has no candidate in-edge).
+// Candidate edges form vertex-disjoint paths; resolving every path by the greedy
+// trie walk (one thread per path) reproduces the DFS's partition exactly, in any
+// order.  Any hazard (a candidate edge into a node of in-degree >= 2 -- a
+// contested or absorbable consumer -- or a parallel edge) sets `hazard` and the
+// ordered DFS replay runs instead.
+__global__ void k_candidates(int V, int R, const int *rule_beg, const int *rule_types, const int *seq_beg,
+                             const int *seq_types, const int *indeg, const int *obeg, const int *odst, int *cnext,
+                             int *cin, int *hazard) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x) {
+        const int a = obeg[t], b = obeg[t + 1];
+        cnext[t] = -1;
+        for (int q = a; q + 1 < b; ++q)
+            if (odst[q] == odst[q + 1]) atomicExch(hazard, 1);  // parallel edges (odst sorted per source)
+        if (b - a != 1) continue;
+        const int w = odst[a];
+        const int ta = seq_beg[t], lt = seq_beg[t + 1] - ta;
+        const int wa = seq_beg[w], lw = seq_beg[w + 1] - wa;
+        bool ok = false;
+        for (int r = 0; r < R && !ok; ++r) {
+            const int pa = rule_beg[r], lp = rule_beg[r + 1] - pa;
+            for (int i = 0; i + lt + lw <= lp && !ok; ++i) {
+                bool m = true;
+                for (int k = 0; k < lt && m; ++k) m = rule_types[pa + i + k] == seq_types[ta + k];
+                for (int k = 0; k < lw && m; ++k) m = rule_types[pa + i + lt + k] == seq_types[wa + k];
+                ok = m;
+            }
+        }
+        if (!ok) continue;
+        cnext[t] = w;
+        cin[w] = 1;
+        if (indeg[w] >= 2) atomicExch(hazard, 1);
+    }
+}
+
+// One thread per candidate path (a node with a candidate out-edge and none in):
+// the DFS's greedy extension (fusion.py:289-298 as replayed by dfs_run) along the
+// path, closing a group whenever the trie walk fails; writes the partition in
+// the DfsState form the final partition reads (where / head / tail / next / tag).
+__global__ void k_chains(int V, int Lmax, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
+                         const int *cnext, const int *cin, const int *hazard, DfsState s) {
+    if (*hazard != 0) return;
+    for (int x0 = blockIdx.x * blockDim.x + threadIdx.x; x0 < V; x0 += gridDim.x * blockDim.x) {
+        if (cnext[x0] < 0 || cin[x0]) continue;
+        int head = x0, tail = x0, gmin = x0, size = 1;
+        int st = s.state[x0], len = s.len[x0], tag = tag_in[x0];
+        auto close = [&]() {
+            if (size < 2) return;
+            for (int y = head;; y = s.next[y]) {
+                s.where[y] = gmin;
+                if (y == tail) break;
+            }
+            s.head[gmin] = head;
+            s.tail[gmin] = tail;
+            s.tag[gmin] = tag;
+        };
+        for (int steps = 0; steps < V; ++steps) {
+            const int w = cnext[tail];
+            if (w < 0) break;
+            const int wa = seq_beg[w], ln = seq_beg[w + 1] - wa;
+            int st2 = st, kind = 0;
+            if (st >= 0 && ln <= Lmax && len + ln <= Lmax) {
+                for (int q = 0; q < ln && st2 >= 0; ++q) st2 = trie_step(t, st2, seq_types[wa + q]);
+                if (st2 >= 0) kind = (t.flags[st2] & 2) ? kTagBound : ((t.flags[st2] & 1) ? kTagFused : 0);
+            }
+            if (kind) {  // combine(cur, nxt) (fusion.py:169-190)
+                s.next[tail] = w;
+                tail = w;
+                gmin = w < gmin ? w : gmin;
+                ++size;
+                st = st2;
+                len += ln;
+                tag = kind;
+            } else {     // the chain stops at `tail`; w heads the next group
+                close();
+                head = tail = gmin = w;
+                size = 1;
+                st = s.state[w];
+                len = s.len[w];
+                tag = tag_in[w];
+            }
+        }
+        close();
+    }
 }
 
 // Distinct current groups of the input successors of `t`, excluding `self`
@@ -416,8 +527,8 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
 
 __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
                       int *stack, int *buf,
-                      int use_vl) {
-    if (threadIdx.x >= 32 || blockIdx.x != 0) return;
+                      int use_vl, const int *hazard) {
+    if (threadIdx.x >= 32 || blockIdx.x != 0 || *hazard == 0) return;  // hazard-free: k_chains resolved it
     if (!use_vl) {
         dfs_run<false>(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
         return;
@@ -436,7 +547,9 @@ __global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const 
 // CTA), the DFS runs on warp 0 at shared-memory latency, and the state is
 // written back for the parallel final partition.
 __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int TN, const int *indeg, const int *obeg,
-                                                   const int *odst, Trie tg, DfsState sg, int stack_cap, int *seen) {
+                                                   const int *odst, Trie tg, DfsState sg, int stack_cap, int *seen,
+                                                   const int *hazard, const int *descending) {
+    if (*hazard == 0) return;  // hazard-free: k_chains resolved it, k_kahn checked cycles
     extern __shared__ __align__(16) int smi[];
     int *p = smi;
     auto take = [&](int n) {
@@ -489,8 +602,12 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
     }
     __syncthreads();
     // Kahn from the sources (graph.py:274-288) on the shared-memory CSR, level by
-    // level (stack = remaining in-degrees, buf = the queue); *seen < V means a cycle
+    // level (stack = remaining in-degrees, buf = the queue); *seen < V means a cycle.
+    // Skipped when every edge ascends in index order (acyclic by construction).
     __shared__ int s_tail;
+    if (*descending == 0) {
+        if (threadIdx.x == 0) *seen = V;
+    } else {
     for (int i = threadIdx.x; i < V; i += blockDim.x) stack[i] = ind[i];
     if (threadIdx.x == 0) s_tail = 0;
     __syncthreads();
@@ -510,6 +627,7 @@ __global__ void __launch_bounds__(1024) k_dfs_smem(int V, int E, int Lmax, int T
         __syncthreads();
     }
     if (threadIdx.x == 0) *seen = s_tail;
+    }
     __syncthreads();
     if (threadIdx.x < 32) dfs_run<false>(V, Lmax, ind, ob, od, t, s, stack, buf);  // warp 0
     __syncthreads();
@@ -823,7 +941,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
                                    std::max(E, 1));
     const size_t tmpb = std::max(std::max(tmp_bytes, t2), std::max(t3, t4)) + 256;
     size_t need = up_used + tmpb + 96 * 512;
-    need += 4ULL * ((V + 1ULL) * 42 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
+    need += 4ULL * ((V + 1ULL) * 44 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
     need += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
     if (cx.dev_cap < need) {
         if (cx.dev) cudaFree(cx.dev);
@@ -858,14 +976,15 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     int *indeg = ar.take<int>(V + 1), *outcnt = ar.take<int>(V + 1), *obeg = ar.take<int>(V + 1);
     int *odst = ar.take<int>(E);
     int *deg = ar.take<int>(V + 1), *fa = ar.take<int>(V + 1), *fb = ar.take<int>(V + 1);
-    int *counters = ar.take<int>(16);  // [0] kahn seen, [1] unique quotient edges
+    int *counters = ar.take<int>(16);  // [0] kahn seen, [1] unique quotient edges, [2] internal edges,
+                                       // [8] order hazard, [9] an edge not ascending in index order
     void *tmp = ar.take<unsigned char>(tmpb);
     CK(cudaMemsetAsync(indeg, 0, 4ULL * (V + 1), st));
     CK(cudaMemsetAsync(outcnt, 0, 4ULL * (V + 1), st));
     CK(cudaMemsetAsync(counters, 0, 64, st));
     size_t tb;
     if (E) {
-        k_make_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, keys, indeg);
+        k_make_keys<<<grid, 256, 0, st>>>(E, d_esrc, d_edst, keys, indeg, counters + 9);
         ++g_mp_launches;
         tb = tmpb;
         CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, skeys, E, 0, 64, st));
@@ -889,7 +1008,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
         CK(cudaEventRecord(cx.ev_fork, st));
         CK(cudaStreamWaitEvent(cx.side, cx.ev_fork, 0));
         CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, cx.side));
-        k_kahn<<<1, 1024, 0, cx.side>>>(V, obeg, odst, deg, fa, fb, counters);
+        k_kahn<<<1, 1024, 0, cx.side>>>(V, obeg, odst, deg, fa, fb, counters, nullptr, counters + 9);
         ++g_mp_launches;
         CK(cudaEventRecord(cx.ev_join, cx.side));
     }
@@ -917,13 +1036,29 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     ++g_mp_launches;
     k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, obeg, s);
     ++g_mp_launches;
+    // K1p: the hazard test and, on hazard-free graphs, the parallel resolution;
+    // exactly one of k_chains / the DFS replay does work (the flag stays on the device)
+    int *hazard = counters + 8;  // [2] is k_edge_keys' count
+    int *cnext = ar.take<int>(V), *cin = ar.take<int>(V);
+    CK(cudaMemsetAsync(cin, 0, 4ULL * V, st));
+    k_candidates<<<grid, 256, 0, st>>>(V, R, d_rbeg, d_rt, d_seq_beg, d_seq, indeg, obeg, odst, cnext, cin, hazard);
+    ++g_mp_launches;
+    k_chains<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, cnext, cin, hazard, s);
+    ++g_mp_launches;
+    if (dfs_in_smem) {
+        // Kahn for the hazard-free case (the shared-memory DFS kernel runs it otherwise)
+        CK(cudaMemcpyAsync(deg, indeg, 4ULL * V, cudaMemcpyDeviceToDevice, st));
+        k_kahn<<<1, 1024, 0, st>>>(V, obeg, odst, deg, fa, fb, counters, hazard, counters + 9);
+        ++g_mp_launches;
+    }
     if (dfs_in_smem) {
         if (!cx.smem_attr) {
             CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs_smem),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
             cx.smem_attr = true;
         }
-        k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap, counters);
+        k_dfs_smem<<<1, 1024, dsm, st>>>(V, E, Lmax, TN, indeg, obeg, odst, trie, s, stack_cap, counters, hazard,
+                                         counters + 9);
     } else {
         // one warp walks an L2-resident state; the visited flags and lengths (one byte
         // per group) sit in shared memory when they fit, the rest of the SM's unified
@@ -934,7 +1069,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
             cx.dfs_attr = true;
         }
-        k_dfs<<<1, 32, use_vl ? V : 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf, use_vl ? 1 : 0);
+        k_dfs<<<1, 32, use_vl ? V : 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf, use_vl ? 1 : 0, hazard);
     }
     ++g_mp_launches;
 
@@ -1012,6 +1147,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
     if (nu > 0 && reinterpret_cast<const unsigned long long *>(pin + p_ukey)[nu - 1] == ~0ULL) --nu;
     out->n_groups = ng;
     out->n_edges = nu;
+    out->ordered_replay = cnt[8] != 0 ? 1 : 0;
     out->grp_node = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
     out->grp_tag = static_cast<int32_t *>(malloc(4ULL * std::max(ng, 1)));
     out->mem_beg = static_cast<int32_t *>(malloc(4ULL * (ng + 1)));

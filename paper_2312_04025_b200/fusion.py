@@ -192,6 +192,11 @@ class _Flat:
             1 if sys.version_info >= (3, 12) else 0)
 
 
+# diagnostics of the last gcof call: ordered_replay = the graph had DFS-order
+# hazards and the ordered replay ran (False: chains resolved in parallel)
+LAST_GCOF: dict = {}
+
+
 def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = None,
          device: int = 0) -> CompGraph:
     """GCOF coarsening on the GPU (``fusion.py:271-304``).
@@ -212,6 +217,7 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         ids = g.node_ids
         raise CycleError(find_cycle(ids, {i: g.succs(i) for i in ids}))
     N.check(code, err, "mp_coarsen")
+    LAST_GCOF["ordered_replay"] = bool(out.ordered_replay)
     try:
         nodes_in = g.nodes
         ng, ne = out.n_groups, out.n_edges

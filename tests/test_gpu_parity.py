@@ -121,6 +121,26 @@ def test_gcof_matches_golden(chunk):
         assert [[e.src, e.dst, e.payload_bytes] for e in out.edges] == case["out"]["edges"], case["name"]
 
 
+def test_gcof_parallel_and_ordered_paths_both_run_on_goldens():
+    """Hazard-free graphs (every candidate edge enters a node of in-degree 1) are
+    resolved by the parallel chain walk, the others by the ordered DFS replay
+    (DESIGN.md §5.2); both paths appear among the goldens, which all match above."""
+    from paper_2312_04025_b200.fusion import LAST_GCOF
+
+    seen = {True: 0, False: 0}
+    for case in golden("gcof.json"):
+        mp.gcof(graph_from(case["graph"]), rules_from(case["rules"]), overrides_from(case.get("overrides")))
+        seen[LAST_GCOF["ordered_replay"]] += 1
+    assert seen[True] >= 50 and seen[False] >= 250, seen  # both paths, every golden matched above
+    for fn in (lambda: workloads.c2(4), workloads.c3, workloads.c4):  # the transformer templates
+        w = fn()
+        mp.gcof(w.raw, w.rules)
+        assert LAST_GCOF["ordered_replay"] is False, w.name
+    w = workloads.c1()
+    mp.gcof(w.raw, w.rules)
+    assert LAST_GCOF["ordered_replay"] is True  # contested consumers (SURVEY App. B)
+
+
 def test_gcof_rejects_cycles_and_is_idempotent():
     rules = workloads.table_rules()
     cyc = mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0}), mp.OpNode(2, "bn", 1, {0: 1.0})],
