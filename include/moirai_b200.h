@@ -109,6 +109,8 @@ typedef struct mp_instance_info {
     int32_t tpp_threads;        /* placements per CTA of the thread-per-placement kernel */
     int32_t tpp_kind;           /* 1: ready set in registers, 2: in shared memory            */
     int32_t ls_ready_cap;       /* local search: proposals whose ready set exceeds it are rejected */
+    int32_t dur_classes;        /* >0: crossing-flow durations come from a table of this many
+                                   distinct payloads x K x K IEEE quotients (0: divided at run time) */
 } mp_instance_info;
 
 /* ---- library ------------------------------------------------------------ */
@@ -132,6 +134,8 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
                                calibrated peak fits a 4/8/16 template) instead of shared memory */
 #define MP_TUNE_OFFCHIP 8   /* group kernel with per-placement state in global memory */
 #define MP_TUNE_TPP_ROUND1 16 /* thread-per-placement: the round-1 shared-memory-ready-set evaluator (A/B only) */
+#define MP_TUNE_NO_DURTAB 32 /* thread-per-placement: divide payload / bw at run time instead of
+                               reading the flow-duration table (A/B and parity tests) */
 #define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernels (used only with
                                automatic G/U) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,

@@ -69,7 +69,7 @@ class mp_instance_info(C.Structure):
         ("fastdiv", C.c_int32),
         ("table_bytes", C.c_int64), ("state_bytes", C.c_int64),
         ("tpp_ready_cap", C.c_int32), ("tpp_threads", C.c_int32), ("tpp_kind", C.c_int32),
-        ("ls_ready_cap", C.c_int32),
+        ("ls_ready_cap", C.c_int32), ("dur_classes", C.c_int32),
     ]
 
 

@@ -299,7 +299,7 @@ int flow_tables(const InstView &V, std::vector<uint32_t> &fsrc, std::vector<uint
             memcpy(&w, &srec[q].x, 8);
             const uint32_t f = static_cast<uint32_t>(w >> 32) - static_cast<uint32_t>(n);
             fsrc[f] = static_cast<uint32_t>(i);
-            fdst[f] = static_cast<uint32_t>(w & 0xffffffffULL);
+            fdst[f] = static_cast<uint32_t>(w) & MP_NODE_MASK;  // bits 20-31: duration-table base
             pay[f] = srec[q].y;
         }
     }

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kBnbThreads) k_bnb_bound(const __grid_constant
                     const int qe = static_cast<int>(out_beg[i + 1]);
                     for (int q = static_cast<int>(out_beg[i]); q < qe; ++q) {
                         const double2 r = rec[q];
-                        const int j = static_cast<int>(static_cast<uint32_t>(dbits(r.x)));
+                        const int j = static_cast<int>(static_cast<uint32_t>(dbits(r.x)) & MP_NODE_MASK);
                         const int dj = j == i0 ? k : prow[j];
                         double wq = 0.0;
                         if (di != 255 && dj != 255 && di != dj)

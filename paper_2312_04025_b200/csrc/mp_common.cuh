@@ -26,7 +26,8 @@ struct TabOff {
     uint32_t mem;       // i64 [n_ops]      mem_bytes                     (solver.py:60)
     uint32_t bw;        // f64 [K*K]        effective bandwidth           (solver.py:66-67)
     uint32_t rbw;       // f64 [K*K]        correctly rounded 1/bw (Markstein division)
-    uint32_t s_rec;     // 16 B [n_flows]   slot record {dst op, node id (n_ops + f), (double)payload}
+    uint32_t s_rec;     // 16 B [n_flows]   slot record {dst op | duration-table base << 20, node id (n_ops + f),
+                        //                  (double)payload}; readers mask the dst op with MP_NODE_MASK
     uint32_t cap;       // i64 [K]          device capacity               (solver.py:59)
     uint32_t out_beg;   // u32 [n_ops+1]    CSR over out-flow *slots* (flows stably sorted by source)
     uint32_t fdst;      // u32 [n_flows]    flow index -> destination op   (solver.py:64)
@@ -37,6 +38,9 @@ struct TabOff {
     uint32_t lvl_beg;   // u32 [n_ops+1]    level offsets into lvl_ops
     uint32_t srcs;      // u32 [n_ops]      ops with no in-flow (initial ready set, solver.py:111)
     uint32_t fpay;      // f64 [n_flows]    payload by flow index (durations recomputed at commit)
+    uint32_t fdur;      // f64 [n_cls*K*K]  flow-duration table: payload class c, pair (a, b) at c*K*K + a*K + b
+                        //                  = (double)payload_c / bw[a][b] (IEEE, solver.py:93-96); 0 on the diagonal
+    uint32_t fcb;       // u32 [n_flows]    duration-table base c*K*K of each flow (by flow index)
     uint32_t bytes;     // total, multiple of 16
 };
 
@@ -67,6 +71,7 @@ struct EvalArgs {
     int n_ops, n_flows, K, n_levels, n_src, n_multi, rcap;
     int colo;                     // skip co-located flows (exact when all durations > 0)
     int fastdiv;                  // payload/bw via verified reciprocal + one Markstein correction
+    int durtab;                   // flow durations read from the to.fdur table (few distinct payloads)
 
     // row source
     const uint8_t *rows;          // LOAD: [n_rows][n_ops]
@@ -235,6 +240,9 @@ cudaError_t mp_eval_set_smem_limits();
 // Thread-per-placement evaluator (mp_eval.cu mp_tpp_kernel): `rc` ready entries
 // held in registers (4, 8 or 16), `threads` placements per CTA.
 #define MP_TPP_MAX_THREADS 512
+// thread-per-placement kernels: their static shared memory is 264 bytes (mbarrier +
+// per-warp keep-best records), so the dynamic part may take the rest of the 227 KB
+#define MP_TPP_SMEM_MAX (MP_SMEM_OPTIN_MAX - 512)
 cudaError_t mp_launch_tpp(int rc, int threads, int ctas, int smem, const EvalArgs &a, cudaStream_t s);
 cudaError_t mp_launch_tpp_ls(int rc, int threads, int ctas, int smem, const EvalArgs &a, const LsArgs &ls,
                              cudaStream_t s);

@@ -208,7 +208,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int qe = static_cast<int>(T_out_beg[i + 1]);
             for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
                 const double2 rec = T_rec[q];
-                const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+                const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)) & MP_NODE_MASK);
                 const int dj = dev[j];
                 // rank of the flow node = dur + rank[j]   (rank[j] >= +0.0)
                 const bool cross = dj != d;
@@ -355,7 +355,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const int q = (act && isop) ? ob + t : 0;
             const double2 rec = T_rec[q];
             const unsigned long long rb = dbits(rec.x);
-            const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+            const int j = static_cast<int>(isop ? (static_cast<uint32_t>(rb) & MP_NODE_MASK) : jflow);
             int dj = 0;
             double rj = 0.0;
             if (act) {  // predicated: idle lanes issue no state loads
@@ -768,6 +768,8 @@ struct TppView {
     // duration is recomputed for the winner only
     unsigned long long *rE, *rR, *rM;  // est bits, rank bits, meta | tie << 32
     const double *T_fpay;              // payload by flow index
+    const double *T_fdur;              // flow-duration table (EvalArgs::durtab)
+    const uint32_t *T_fcb;             // its base by flow index
 };
 
 // nib: the row tile holds two device indices per byte (shared-memory ready-set
@@ -812,6 +814,8 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.rR = v.rE + rdy;
     v.rM = v.rR + rdy;
     v.T_fpay = tab<double>(tb, a.to.fpay);
+    v.T_fdur = tab<double>(tb, a.to.fdur);
+    v.T_fcb = tab<uint32_t>(tb, a.to.fcb);
     return v;
 }
 
@@ -928,7 +932,7 @@ __device__ __forceinline__ TppResult tpp_eval(const TppView &v, const EvalArgs &
         const int qe = static_cast<int>(T_out_beg[i + 1]);
         for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
             const double2 rec = T_rec[q];
-            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)) & MP_NODE_MASK);
             const int dj = rowt[j * T + tid];
             const bool cross = dj != d;
             const int bi = cross ? d * K + dj : 0;
@@ -1057,7 +1061,7 @@ __device__ __forceinline__ TppResult tpp_eval(const TppView &v, const EvalArgs &
                 const int q = (act && isop) ? ob + t : 0;
                 const double2 rec = T_rec[q];
                 const unsigned long long rb = dbits(rec.x);
-                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                const int j = static_cast<int>(isop ? (static_cast<uint32_t>(rb) & MP_NODE_MASK) : jflow);
                 j_[u] = j;
                 dj_[u] = rowt[j * T + tid];
                 pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
@@ -1190,7 +1194,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
         const int qe = static_cast<int>(T_out_beg[i + 1]);
         for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
             const double2 rec = T_rec[q];
-            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)) & MP_NODE_MASK);
             const int dj = dev(j);
             const bool cross = dj != d;
             const int bi = cross ? d * K + dj : 0;
@@ -1291,7 +1295,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
                 const int q = (act && isop) ? ob + t : 0;
                 const double2 rec = T_rec[q];
                 const unsigned long long rb = dbits(rec.x);
-                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                const int j = static_cast<int>(isop ? (static_cast<uint32_t>(rb) & MP_NODE_MASK) : jflow);
                 j_[u] = j;
                 dj_[u] = dev(j);
                 pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
@@ -1411,7 +1415,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
 //     64-bit word, so a consumer update is one 8-byte and one 16-byte round trip.
 // Global per-lane state (lane-interleaved [index][L], tpp_state_bytes): rank f64
 // [n_ops], est f64 [n_multi], tie | npred << 32 u64 [n_multi].
-template <bool COLO>
+template <bool COLO, bool TAB>
 __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs &a, bool live, bool bad, int cap) {
     const int T = v.T, n_ops = v.n_ops, K = v.K;
     const unsigned char *__restrict__ rowl = v.rowt + v.tid;  // op x: rowl[(x >> 1) * T], nibble (x & 1)
@@ -1421,16 +1425,14 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     const long long gl = static_cast<long long>(blockIdx.x) * T + v.tid;
     unsigned char *g0 = a.gstate + gl * 8;
     unsigned char *__restrict__ g_rank = g0;
-    unsigned char *__restrict__ g_mest = g0 + static_cast<long long>(n_ops) * v.L * 8;
-    unsigned char *__restrict__ g_mtn = g0 + static_cast<long long>(n_ops + a.n_multi) * v.L * 8;
+    // multi-input op state: one 16-byte record {est, tie | npred << 32} per (op, lane)
+    unsigned char *__restrict__ g_m = a.gstate + static_cast<long long>(n_ops) * v.L * 8 + gl * 16;
+    const unsigned L16 = L8 * 2u;
     auto grank = [&](int j) -> double * {
         return reinterpret_cast<double *>(g_rank + static_cast<unsigned long long>(static_cast<unsigned>(j) * L8));
     };
-    auto gmest = [&](unsigned k) -> double * {
-        return reinterpret_cast<double *>(g_mest + static_cast<unsigned long long>(k * L8));
-    };
-    auto gmtn = [&](unsigned k) -> unsigned long long * {
-        return reinterpret_cast<unsigned long long *>(g_mtn + static_cast<unsigned long long>(k * L8));
+    auto gm = [&](unsigned k) -> double2 * {
+        return reinterpret_cast<double2 *>(g_m + static_cast<unsigned long long>(k * L16));
     };
     const double *__restrict__ T_cost = v.T_cost;
     const long long *__restrict__ T_mem = v.T_mem;
@@ -1446,6 +1448,8 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     const uint32_t *__restrict__ T_mdeg = v.T_mdeg;
     const uint32_t *__restrict__ T_mop = v.T_mop;
     const double *__restrict__ T_fpay = v.T_fpay;
+    const double *__restrict__ T_fdur = v.T_fdur;  // TAB: flow durations by (class, pair)
+    const uint32_t *__restrict__ T_fcb = v.T_fcb;   // TAB: class base by flow index
     const int fast = v.fast;
     const uint32_t RZ = v.RZ, WS = v.WS;
     const int capA = (a.rcap + 1) & ~1;
@@ -1481,11 +1485,15 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         const int qe = static_cast<int>(T_out_beg[i + 1]);
         for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
             const double2 rec = T_rec[q];
-            const int j = static_cast<int>(static_cast<uint32_t>(dbits(rec.x)));
+            const uint32_t lo = static_cast<uint32_t>(dbits(rec.x));
+            const int j = static_cast<int>(lo & MP_NODE_MASK);
             const int dj = dev(j);
             const double rj = *grank(j);
             double fr = rj;
-            if (dj != d) {  // warp-divergent only in timing: both sides are short
+            if constexpr (TAB) {
+                const double du = T_fdur[(lo >> MP_NODE_BITS) + d * K + dj];
+                fr = dj != d ? du + rj : rj;
+            } else if (dj != d) {  // warp-divergent only in timing: both sides are short
                 const int bi = d * K + dj;
                 fr = div_bw(rec.y, T_bw[bi], T_rbw[bi], fast) + rj;
             }
@@ -1495,10 +1503,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     }
 
     // ---- 4. dispatch state (solver.py:109-116) -----------------------------------------
-    for (int k = 0; k < a.n_multi; ++k) {
-        *gmtn(k) = static_cast<unsigned long long>(T_mop[k]) | (static_cast<unsigned long long>(T_mdeg[k]) << 32);
-        *gmest(k) = 0.0;
-    }
+    for (int k = 0; k < a.n_multi; ++k)
+        *gm(k) = make_double2(0.0, bitsd(static_cast<unsigned long long>(T_mop[k]) |
+                                         (static_cast<unsigned long long>(T_mdeg[k]) << 32)));
     for (int k = 0; k <= static_cast<int>(WS); ++k) clk[k * T] = 0.0;
     const unsigned long long NAN_BITS = 0xfff8000000000000ULL;
     const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (RZ << 20) | (RZ << 26));
@@ -1575,7 +1582,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         // (none of which writes what they read)
         constexpr int SU = 2;
         int j_[SU], dj_[SU];
-        uint32_t pid_[SU], k_[SU];
+        uint32_t pid_[SU], k_[SU], cb_[SU];
         unsigned long long tn_[SU];
         double rj_[SU], cur_[SU], pay_[SU];
         bool act_[SU];
@@ -1586,11 +1593,15 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 const bool act = t < cnt;
                 const double2 rec = T_rec[(act & isop) ? ob + t : 0];
                 const unsigned long long rb = dbits(rec.x);
-                const int j = static_cast<int>(isop ? static_cast<uint32_t>(rb) : jflow);
+                const int j = static_cast<int>(isop ? (static_cast<uint32_t>(rb) & MP_NODE_MASK) : jflow);
                 j_[u] = j;
                 dj_[u] = dev(j);
                 pid_[u] = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
-                pay_[u] = rec.y;
+                if constexpr (TAB) {
+                    cb_[u] = static_cast<uint32_t>(rb) >> MP_NODE_BITS;
+                } else {
+                    pay_[u] = rec.y;
+                }
                 act_[u] = act;
                 rj_[u] = *grank(j);
                 const uint32_t k = T_mi[j];
@@ -1599,8 +1610,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 tn_[u] = 1ULL << 32;
                 cur_[u] = 0.0;
                 if (op_upd & (k != MP_NONE)) {
-                    tn_[u] = *gmtn(k);
-                    cur_[u] = *gmest(k);
+                    const double2 ms2 = *gm(k);
+                    cur_[u] = ms2.x;
+                    tn_[u] = dbits(ms2.y);
                 }
             }
         };
@@ -1612,7 +1624,11 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
             bd = T_cost[node * K + d];
         } else if (!done && r1 != RZ) {
             const int bi2 = (d - K) * K + (static_cast<int>(r2) - 2 * K);
-            bd = div_bw(T_fpay[node - n_ops], T_bw[bi2], T_rbw[bi2], fast);
+            if constexpr (TAB) {
+                bd = T_fdur[T_fcb[node - n_ops] + bi2];
+            } else {
+                bd = div_bw(T_fpay[node - n_ops], T_bw[bi2], T_rbw[bi2], fast);
+            }
         }
         // unordered removal: the last entry moves into the hole, the vacated slot
         // becomes NaN (never taken)
@@ -1649,8 +1665,14 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 const bool via_colo = COLO & isop & !cross;
                 const bool flow_ins = act & isop & !via_colo;  // a flow enters the ready set
                 const bool op_upd = act & !flow_ins;           // j's npred / est / gate change
-                const int bi2 = cross ? d * K + dj : 0;         // computed unconditionally, selected
-                const double fdur = (isop & cross) ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                double fdur;
+                if constexpr (TAB) {  // the table's diagonal is 0.0
+                    const double du = T_fdur[cb_[u] + d * K + dj];
+                    fdur = isop ? du : 0.0;
+                } else {
+                    const int bi2 = cross ? d * K + dj : 0;     // computed unconditionally, selected
+                    fdur = (isop & cross) ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                }
                 const double rj = rj_[u];
                 const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
                                                        (static_cast<uint32_t>(2 * K + dj) << 26))
@@ -1663,10 +1685,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 const bool up = end > cur;
                 const double ej = multi ? (up ? end : cur) : end;
                 const uint32_t tie_new = up ? tj : ((via_colo & (end == cur) & (pid > ct)) ? pid : ct);
-                if (op_upd & multi) {
-                    *gmtn(k_[u]) = static_cast<unsigned long long>(tie_new) | (static_cast<unsigned long long>(np) << 32);
-                    *gmest(k_[u]) = ej;
-                }
+                if (op_upd & multi)
+                    *gm(k_[u]) = make_double2(ej, bitsd(static_cast<unsigned long long>(tie_new) |
+                                                        (static_cast<unsigned long long>(np) << 32)));
                 const bool op_ins = op_upd & (!multi | (np == 0u));
                 insert(flow_ins | op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
                        flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
@@ -1806,7 +1827,9 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
         const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
         const long long grow = a.row_base + lrow;
         const bool bad = tpp_load_row<true>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
-        const TppResult r = VAR == 1 ? tpps_eval<COLO>(v, a, live, bad, a.rcap) : tpp2_eval<COLO>(v, a, live, bad, a.rcap);
+        const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, bad, a.rcap)
+                            : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, bad, a.rcap)
+                                       : tpp2_eval<COLO, false>(v, a, live, bad, a.rcap);
         if (live) {
             const long long o = grow - a.out_base;
             if (r.ovf) {
@@ -1852,7 +1875,9 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
         const long long srow = live ? static_cast<long long>(gc % static_cast<unsigned long long>(ls.n_seed)) : 0;
         tpp_load_row<true>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
-        const TppResult r0 = VAR == 1 ? tpps_eval<COLO>(v, a, live, false, a.rcap) : tpp2_eval<COLO>(v, a, live, false, a.rcap);
+        const TppResult r0 = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
+                             : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
+                                        : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
         double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
@@ -1862,7 +1887,9 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
             const int old = (*cell >> sh) & 15;
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
             if (live) *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (nd << sh));
-            const TppResult r = VAR == 1 ? tpps_eval<COLO>(v, a, live, false, a.rcap) : tpp2_eval<COLO>(v, a, live, false, a.rcap);
+            const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
+                                : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
+                                           : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
                 cur_ms = ms;
@@ -2033,7 +2060,7 @@ template <typename F>
 cudaError_t tpp_attr(F *const (&fs)[6]) {
     for (F *f : fs) {
         cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -2079,15 +2106,16 @@ cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, c
     static bool attr = false;
     if (!attr) {
         for (EvalFn f : {mp_tpps_kernel<true, 0>, mp_tpps_kernel<false, 0>, mp_tpps_kernel<true, 1>,
-                         mp_tpps_kernel<false, 1>}) {
+                         mp_tpps_kernel<false, 1>, mp_tpps_kernel<true, 2>, mp_tpps_kernel<false, 2>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
     EvalFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_kernel<true, 1> : mp_tpps_kernel<false, 1>)
-                              : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>);
+               : a.durtab    ? (a.colo ? mp_tpps_kernel<true, 2> : mp_tpps_kernel<false, 2>)
+                             : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
@@ -2097,15 +2125,16 @@ cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a
     static bool attr = false;
     if (!attr) {
         for (LsFn f : {mp_tpps_ls_kernel<true, 0>, mp_tpps_ls_kernel<false, 0>, mp_tpps_ls_kernel<true, 1>,
-                       mp_tpps_ls_kernel<false, 1>}) {
+                       mp_tpps_ls_kernel<false, 1>, mp_tpps_ls_kernel<true, 2>, mp_tpps_ls_kernel<false, 2>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX);
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
     LsFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_ls_kernel<true, 1> : mp_tpps_ls_kernel<false, 1>)
-                            : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>);
+             : a.durtab    ? (a.colo ? mp_tpps_ls_kernel<true, 2> : mp_tpps_ls_kernel<false, 2>)
+                           : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();

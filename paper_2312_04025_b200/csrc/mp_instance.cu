@@ -27,6 +27,7 @@
 namespace {
 
 constexpr int kBuildThreads = 1024;
+constexpr long long kDurTabMax = 2048;  // flow-duration table cells (16 KB of shared memory; base fits 12 bits)
 
 inline double __longlong_as_double_host(unsigned long long b) {
     double d;
@@ -121,11 +122,14 @@ __global__ void k_copy_validate(int n_ops, int n_flows, int K, const double *cos
 }
 
 // flow slots in source order: one 16-byte record {dst | node id << 32, payload}
+// (with the flow-duration table, bits 20-31 of the low word hold the flow's table base)
 __global__ void k_slots(int n_ops, int n_flows, const unsigned int *sorted_f, const int *fdst, const double *pay_d,
-                        unsigned char *blob, TabOff to) {
+                        unsigned char *blob, TabOff to, int durtab) {
+    const uint32_t *fcb = reinterpret_cast<const uint32_t *>(blob + to.fcb);
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_flows; q += gridDim.x * blockDim.x) {
         const unsigned int f = sorted_f[q];
-        const unsigned long long w = static_cast<unsigned long long>(static_cast<uint32_t>(fdst[f])) |
+        const uint32_t lo = static_cast<uint32_t>(fdst[f]) | (durtab ? fcb[f] << MP_NODE_BITS : 0u);
+        const unsigned long long w = static_cast<unsigned long long>(lo) |
                                      (static_cast<unsigned long long>(static_cast<uint32_t>(n_ops) + f) << 32);
         reinterpret_cast<double2 *>(blob + to.s_rec)[q] = make_double2(__longlong_as_double(static_cast<long long>(w)), pay_d[f]);
     }
@@ -281,7 +285,7 @@ StOff make_stoff(int n_ops, int n_multi, int K, int rcap) {
     return s;
 }
 
-TabOff make_taboff(int n_ops, int n_flows, int K) {
+TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls) {
     TabOff t{};
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) {
@@ -304,6 +308,8 @@ TabOff make_taboff(int n_ops, int n_flows, int K) {
     t.lvl_beg = take(4ULL * (n_ops + 1));
     t.srcs = take(4ULL * n_ops);
     t.fpay = take(8ULL * n_flows);
+    t.fdur = take(8ULL * n_cls * K * K);
+    t.fcb = take(n_cls > 0 ? 4ULL * n_flows : 0);
     t.bytes = static_cast<uint32_t>(o);
     return t;
 }
@@ -336,6 +342,8 @@ struct mp_instance {
     bool colo = false;     // co-located flows skipped
     bool fastdiv = false;  // Markstein division verified for this instance
     int slow_div_pairs = 0;
+    int dur_classes = 0;   // distinct payloads in the flow-duration table (0: durations divided at run time)
+    bool durtab_off = false;  // MP_TUNE_NO_DURTAB
     int sms = 0;
     int rcap_target = 32;
     int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
@@ -495,7 +503,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     I->tpp_kind = 0;
     if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
         const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
-        const long long avail = static_cast<long long>(smem_cap) - I->to.bytes - 32;
+        const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;
         const long long base_lane = n_ops + 8LL * (3 * K + 2);
         // shared-memory ready set: 24 B per entry per lane, capacity = the peak (>= 4),
         // row tile nibble-packed
@@ -530,7 +538,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
 // thread-per-placement shape with a shared-memory ready set of capacity `cap`
 // (local search runs at the group kernel's capacity); threads = 0 if it does not fit
 void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
-    const long long avail = static_cast<long long>(MP_SMEM_DYN_MAX) - I->to.bytes - 32;
+    const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;
     const long long row = (I->n_ops + 1) / 2;  // nibble-packed row tile
     const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * ((cap + 1) & ~1);  // even slot count
     const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
@@ -564,6 +572,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.n_multi = I->n_multi;
     a.colo = I->colo ? 1 : 0;
     a.fastdiv = I->fastdiv ? 1 : 0;
+    a.durtab = (I->dur_classes > 0 && !I->durtab_off) ? 1 : 0;
     a.tpp_alt = I->tpp_round1 ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
@@ -624,7 +633,35 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     cudaDeviceProp prop{};
     cudaGetDeviceProperties(&prop, device);
     I->sms = prop.multiProcessorCount;
-    I->to = make_taboff(n_ops, n_flows, K);
+    // Flow-duration table: with few distinct payloads (the model graphs: 3-4) every
+    // crossing-flow duration payload / bw[a][b] (solver.py:93-96) is one of
+    // n_cls*K*(K-1) IEEE quotients, computed here once (host and device division are
+    // both correctly rounded) and looked up by the evaluator instead of divided.
+    std::vector<long long> upay;
+    std::vector<uint32_t> h_fcb;
+    std::vector<double> h_fdur;
+    if (n_flows > 0 && K >= 2) {
+        upay.assign(prob->payload, prob->payload + n_flows);
+        std::sort(upay.begin(), upay.end());
+        upay.erase(std::unique(upay.begin(), upay.end()), upay.end());
+        const long long cells = static_cast<long long>(upay.size()) * K * K;
+        if (cells <= kDurTabMax) {
+            h_fdur.assign(static_cast<size_t>(cells), 0.0);
+            for (size_t c = 0; c < upay.size(); ++c)
+                for (int x = 0; x < K; ++x)
+                    for (int y = 0; y < K; ++y)
+                        if (x != y)
+                            h_fdur[c * K * K + x * K + y] = static_cast<double>(upay[c]) / prob->bw[x * K + y];
+            h_fcb.resize(n_flows);
+            for (int f = 0; f < n_flows; ++f)
+                h_fcb[f] = static_cast<uint32_t>(
+                    (std::lower_bound(upay.begin(), upay.end(), prob->payload[f]) - upay.begin()) * K * K);
+        } else {
+            upay.clear();
+        }
+    }
+    const int n_cls = static_cast<int>(h_fcb.empty() ? 0 : upay.size());
+    I->to = make_taboff(n_ops, n_flows, K, n_cls);
 
     auto fail = [&](int code) {
         mp_instance_destroy(I);
@@ -646,6 +683,13 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
     }
     MP_CUDA_I(cudaMalloc(&I->blob, I->to.bytes));
     MP_CUDA_I(cudaMemsetAsync(I->blob, 0, I->to.bytes, I->stream));
+    if (n_cls > 0) {
+        MP_CUDA_I(cudaMemcpyAsync(I->blob + I->to.fdur, h_fdur.data(), 8ULL * h_fdur.size(), cudaMemcpyHostToDevice,
+                                  I->stream));
+        MP_CUDA_I(cudaMemcpyAsync(I->blob + I->to.fcb, h_fcb.data(), 4ULL * n_flows, cudaMemcpyHostToDevice,
+                                  I->stream));
+    }
+    I->dur_classes = n_cls;
 
     // ---- upload raw arrays -------------------------------------------------
     const size_t b_cost = 8ULL * n_ops * K, b_mem = 8ULL * n_ops, b_f = 4ULL * n_flows, b_pay = 8ULL * n_flows,
@@ -765,7 +809,7 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         tb = tmpb;
         MP_CUDA_I(cub::DeviceRadixSort::SortPairs(tmp, tb, reinterpret_cast<const unsigned int *>(raw_src), keys, iota,
                                                   sorted_f, n_flows, 0, 32, I->stream));
-        k_slots<<<gridN, 256, 0, I->stream>>>(n_ops, n_flows, sorted_f, raw_dst, pay_d, I->blob, I->to);
+        k_slots<<<gridN, 256, 0, I->stream>>>(n_ops, n_flows, sorted_f, raw_dst, pay_d, I->blob, I->to, n_cls > 0);
         ++g_mp_launches;
         k_verify_div<<<gridN, 256, 0, I->stream>>>(n_flows, K, pay_d, I->blob, I->to, reinterpret_cast<unsigned int *>(nsel) + 2);
         ++g_mp_launches;
@@ -921,6 +965,7 @@ int32_t mp_instance_info_get(const mp_instance *I, mp_instance_info *info) {
     info->tpp_kind = I->tpp_kind;
     info->ls_ready_cap = I->ls_cap;
     info->tpp_threads = I->tpp_rc > 0 ? I->tpp_threads : 0;
+    info->dur_classes = I->durtab_off ? 0 : I->dur_classes;
     return MP_OK;
 }
 
@@ -941,6 +986,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->tpp_reg_pref = (flags & MP_TUNE_TPP_REG) != 0;
     I->tpp_round1 = (flags & MP_TUNE_TPP_ROUND1) != 0;
     I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
+    I->durtab_off = (flags & MP_TUNE_NO_DURTAB) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }

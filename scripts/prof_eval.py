@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--tpp-reg", action="store_true")
     ap.add_argument("--offchip", action="store_true")
     ap.add_argument("--round1", action="store_true", help="the round-1 TPP evaluator (A/B)")
+    ap.add_argument("--no-durtab", action="store_true", help="divide flow durations at run time (A/B)")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     args = ap.parse_args()
@@ -54,7 +55,8 @@ def main():
     for spec in args.G.split(","):
         G, U = (int(x) for x in (spec.split(":") + ["0"])[:2])
         inst.tune(G, args.ctas_per_sm, ready_cap=args.rcap, colo=not args.no_colo, lanes_used=U, tpp=not args.no_tpp,
-                  tpp_registers=args.tpp_reg, offchip=args.offchip, tpp_round1=args.round1)
+                  tpp_registers=args.tpp_reg, offchip=args.offchip, tpp_round1=args.round1,
+                  durtab=not args.no_durtab)
         info = inst.info()
         best = C.c_int64()
         bms = C.c_double()
@@ -82,7 +84,7 @@ def main():
         feas = int((st == 0).sum().item())
         print(f"{w.name} a={inst.n_ops} b={inst.n_flows} peak={info['peak_probe']} feasible={feas}/{args.rows} G={info['group_lanes']} U={info['lanes_used']} colo={info['colo']} gpc={info['groups_per_cta']} "
               f"ctas={info['ctas']} rcap={info['ready_cap']} smem={info['smem_bytes']} state={info['state_bytes']} "
-              f"mode={info['mode']} tables={info['table_bytes']} tpp={info['tpp_kind']}:{info['tpp_ready_cap']}x{info['tpp_threads']}: {args.rows / t:,.0f} placements/s ({t * 1e3:.2f} ms) best={best.value}",
+              f"mode={info['mode']} tables={info['table_bytes']} durtab={info['dur_classes']} tpp={info['tpp_kind']}:{info['tpp_ready_cap']}x{info['tpp_threads']}: {args.rows / t:,.0f} placements/s ({t * 1e3:.2f} ms), feasible rows scheduled {feas / t:,.0f}/s best={best.value}",
               flush=True)
 
 

@@ -255,13 +255,14 @@ SHAPES = [dict(group_lanes=g, colo=colo, ready_cap=rc) for g in (1, 2, 4, 8, 16,
 # fits its register capacity (4 / 8 / 16 entries; ready_cap=3 forces reruns)
 TPP_SHAPES = [dict(), dict(colo=False), dict(ready_cap=3), dict(ready_cap=6, colo=False), dict(ready_cap=12),
               dict(tpp_registers=True), dict(tpp_registers=True, colo=False), dict(tpp_registers=True, ready_cap=3),
-              dict(tpp_registers=True, ready_cap=12), dict(tpp_round1=True), dict(tpp_round1=True, ready_cap=3)]
+              dict(tpp_registers=True, ready_cap=12), dict(tpp_round1=True), dict(tpp_round1=True, ready_cap=3),
+              dict(durtab=False), dict(durtab=False, colo=False, ready_cap=3)]
 
 
 @pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
 def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
     rng = random.Random({"plain": 1, "tight": 2, "ties": 3, "zero": 4}[flavor])
-    tpp_runs = 0
+    tpp_runs = tab_runs = 0
     for trial in range(6):
         g, c = random_problem(rng, rng.randint(3, 60), rng.randint(2, 5), tight=flavor == "tight",
                               ties=flavor == "ties", zero=flavor == "zero")
@@ -274,6 +275,7 @@ def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
             for shape in SHAPES + TPP_SHAPES:
                 inst.tune(**shape)
                 tpp_runs += inst.info()["tpp_ready_cap"] > 0
+                tab_runs += inst.info()["tpp_ready_cap"] > 0 and inst.info()["dur_classes"] > 0
                 ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
                 assert np.array_equal(st, wst), (flavor, trial, shape)
                 assert np.array_equal(bits(ms), bits(want)), (flavor, trial, shape, inst.info())
@@ -282,6 +284,8 @@ def test_eval_vs_oracle_all_shapes(oracle_mod, flavor):
             if flavor == "zero":
                 assert inst.info()["colo_ok"] in (0, 1)
     assert tpp_runs >= 10, tpp_runs
+    if flavor == "ties":  # one payload value: the flow-duration table is in use
+        assert tab_runs >= 10, tab_runs
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
@@ -294,7 +298,8 @@ def test_eval_vs_oracle_workloads(oracle_mod, name):
         rows = workloads.placements(w.seed, 4096 if name != "c5" else 256, inst.n_ops, inst.K)
         want, wst = orc.eval_batch(rows, threads=8)
         for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False),
-                      dict(ready_cap=3), dict(tpp=False), dict(tpp_registers=True), dict(tpp_round1=True)):
+                      dict(ready_cap=3), dict(tpp=False), dict(tpp_registers=True), dict(tpp_round1=True),
+                      dict(durtab=False)):
             inst.tune(**shape)
             ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
             assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)

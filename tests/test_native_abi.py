@@ -37,8 +37,9 @@ def test_struct_layouts_match_header():
     # spot-check sizes against the header's field lists
     assert C.sizeof(N.mp_error) == 8 + 8 + 8 + 200  # int32 padded to 8, two int64, char[200]
     assert C.sizeof(N.mp_problem) == 16 + 7 * 8
-    # 21 int32 (+ pad) + 2 int64 + 4 int32 (tpp_ready_cap, tpp_threads, tpp_kind, ls_ready_cap)
-    assert C.sizeof(N.mp_instance_info) == 22 * 4 + 2 * 8 + 4 * 4
+    # 21 int32 (+ pad) + 2 int64 + 5 int32 (tpp_ready_cap, tpp_threads, tpp_kind, ls_ready_cap,
+    # dur_classes) + pad
+    assert C.sizeof(N.mp_instance_info) == 22 * 4 + 2 * 8 + 6 * 4
     assert C.sizeof(N.mp_violation) == 4 + 4 + 8 + 8
     assert C.sizeof(N.mp_graph_view) == 3 * 8 + 16 * 8
 
