@@ -37,10 +37,11 @@ struct TabOff {
     uint32_t lvl_ops;   // u32 [n_ops]      ops bucketed by height (0 = sinks)
     uint32_t lvl_beg;   // u32 [n_ops+1]    level offsets into lvl_ops
     uint32_t srcs;      // u32 [n_ops]      ops with no in-flow (initial ready set, solver.py:111)
-    uint32_t fpay;      // f64 [n_flows]    payload by flow index (durations recomputed at commit)
     uint32_t fdur;      // f64 [n_cls*K*K]  flow-duration table: payload class c, pair (a, b) at c*K*K + a*K + b
                         //                  = (double)payload_c / bw[a][b] (IEEE, solver.py:93-96); 0 on the diagonal
     uint32_t fcb;       // u32 [n_flows]    duration-table base c*K*K of each flow (by flow index)
+    uint32_t fpay;      // f64 [n_flows]    payload by flow index (durations recomputed at commit by the
+                        //                  division variants; last, so the table variant stages [0, fpay))
     uint32_t bytes;     // total, multiple of 16
 };
 
@@ -72,6 +73,8 @@ struct EvalArgs {
     int colo;                     // skip co-located flows (exact when all durations > 0)
     int fastdiv;                  // payload/bw via verified reciprocal + one Markstein correction
     int durtab;                   // flow durations read from the to.fdur table (few distinct payloads)
+    uint32_t tpp_stage;           // TPP kernels: table bytes staged into shared memory (to.fpay with the
+                                  // duration table, else to.bytes); the row tile starts there
 
     // row source
     const uint8_t *rows;          // LOAD: [n_rows][n_ops]

@@ -113,17 +113,17 @@ struct RowResult {
 
 // Stage the instance tables into shared memory (one elected thread issues 1-D
 // bulk async copies; every thread waits on the mbarrier's phase 0).
-__device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &a, uint64_t *bar) {
+__device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &a, uint64_t *bar, uint32_t bytes) {
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(bar, a.to.bytes);
+        mbar_arrive_expect_tx(bar, bytes);
         constexpr uint32_t CH = 32768;
-        for (uint32_t off = 0; off < a.to.bytes; off += CH) {
-            const uint32_t n = (a.to.bytes - off < CH) ? (a.to.bytes - off) : CH;
+        for (uint32_t off = 0; off < bytes; off += CH) {
+            const uint32_t n = (bytes - off < CH) ? (bytes - off) : CH;
             bulk_g2s(sm + off, a.blob + off, n, bar);
         }
     }
@@ -473,7 +473,7 @@ template <int MODE>
 __device__ __forceinline__ void group_bases(unsigned char *sm, const EvalArgs &a, int grp, uint64_t *bar,
                                             const unsigned char *&tb, unsigned char *&st) {
     if constexpr (MODE == 2) {
-        stage_tables(sm, a, bar);
+        stage_tables(sm, a, bar, a.to.bytes);
         tb = sm;
         st = sm + a.to.bytes + static_cast<size_t>(grp) * a.so.bytes;
     } else if constexpr (MODE == 1) {
@@ -780,9 +780,9 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.tid = threadIdx.x;
     v.n_ops = a.n_ops;
     v.K = a.K;
-    v.rowt = sm + a.to.bytes;
+    v.rowt = sm + a.tpp_stage;
     const size_t row_bytes = nib ? static_cast<size_t>((a.n_ops + 1) / 2) : static_cast<size_t>(a.n_ops);
-    v.clk = reinterpret_cast<double *>(sm + a.to.bytes + ((row_bytes * v.T + 15) & ~static_cast<size_t>(15)));
+    v.clk = reinterpret_cast<double *>(sm + a.tpp_stage + ((row_bytes * v.T + 15) & ~static_cast<size_t>(15)));
     v.ld = reinterpret_cast<unsigned long long *>(v.clk);
     v.L = a.lane_stride;
     const long long gl = static_cast<long long>(blockIdx.x) * v.T + v.tid;
@@ -1711,7 +1711,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_kernel(const __g
     __shared__ double s_best_ms[MP_TPP_MAX_THREADS / 32];
     __shared__ long long s_best_row[MP_TPP_MAX_THREADS / 32];
     const int lane = threadIdx.x & 31;
-    stage_tables(sm, a, &s_bar);
+    stage_tables(sm, a, &s_bar, a.tpp_stage);
     const TppView v = tpp_view(a, sm);
     const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
     double best_ms = kInf;
@@ -1763,7 +1763,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_ls_kernel(const 
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
     const int lane = threadIdx.x & 31;
-    stage_tables(sm, a, &s_bar);
+    stage_tables(sm, a, &s_bar, a.tpp_stage);
     const TppView v = tpp_view(a, sm);
     const int n = a.n_ops, K = a.K, T = v.T, tid = v.tid;
     for (;;) {
@@ -1808,7 +1808,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
     __shared__ double s_best_ms[MP_TPP_MAX_THREADS / 32];
     __shared__ long long s_best_row[MP_TPP_MAX_THREADS / 32];
     const int lane = threadIdx.x & 31;
-    stage_tables(sm, a, &s_bar);
+    stage_tables(sm, a, &s_bar, a.tpp_stage);
     const TppView v = tpp_view(a, sm, true);
     const long long n_rows = a.n_rows_dev ? static_cast<long long>(*a.n_rows_dev) : a.n_rows;
     double best_ms = kInf;
@@ -1862,7 +1862,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
     const int lane = threadIdx.x & 31;
-    stage_tables(sm, a, &s_bar);
+    stage_tables(sm, a, &s_bar, a.tpp_stage);
     const TppView v = tpp_view(a, sm, true);
     const int n = a.n_ops, K = a.K, T = v.T, tid = v.tid;
     for (;;) {

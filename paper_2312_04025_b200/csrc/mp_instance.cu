@@ -285,7 +285,10 @@ StOff make_stoff(int n_ops, int n_multi, int K, int rcap) {
     return s;
 }
 
-TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls) {
+// n_multi / n_src: ops with >= 2 / no valid in-flows (counted on the host, the same
+// counts the build kernels produce); the fpay section comes last so that the
+// duration-table TPP kernels stage [0, fpay) only
+TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls, int n_multi, int n_src) {
     TabOff t{};
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) {
@@ -302,14 +305,14 @@ TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls) {
     t.s_rec = take(16ULL * n_flows);
     t.fdst = take(4ULL * n_flows);
     t.mi = take(4ULL * n_ops);
-    t.m_op = take(4ULL * n_ops);   // n_multi <= n_ops
-    t.m_deg = take(4ULL * n_ops);
+    t.m_op = take(4ULL * n_multi);
+    t.m_deg = take(4ULL * n_multi);
     t.lvl_ops = take(4ULL * n_ops);
     t.lvl_beg = take(4ULL * (n_ops + 1));
-    t.srcs = take(4ULL * n_ops);
-    t.fpay = take(8ULL * n_flows);
+    t.srcs = take(4ULL * n_src);
     t.fdur = take(8ULL * n_cls * K * K);
     t.fcb = take(n_cls > 0 ? 4ULL * n_flows : 0);
+    t.fpay = take(8ULL * n_flows);
     t.bytes = static_cast<uint32_t>(o);
     return t;
 }
@@ -388,6 +391,7 @@ struct mp_instance {
 namespace {
 
 void set_ls_cap(mp_instance *I, int ready_cap_req);
+uint32_t tpp_tab_bytes(const mp_instance *I);
 
 void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, int ready_cap_req = 0) {
     const int n_ops = I->n_ops, K = I->K;
@@ -503,13 +507,14 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     I->tpp_kind = 0;
     if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
         const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
-        const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;
+        const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;  // register variant
+        const long long avail_s = static_cast<long long>(MP_TPP_SMEM_MAX) - tpp_tab_bytes(I) - 32;
         const long long base_lane = n_ops + 8LL * (3 * K + 2);
         // shared-memory ready set: 24 B per entry per lane, capacity = the peak (>= 4),
         // row tile nibble-packed
         const int cap_s = ready_cap_req > 0 ? rcap : std::min(I->ready_bound, std::max(4, want));
         const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1);
-        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / lane_s) / 32 * 32));
+        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail_s / lane_s) / 32 * 32));
         // register ready set: the smallest template >= the peak
         const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
         const int Tr = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / base_lane) / 32 * 32));
@@ -521,7 +526,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
             I->tpp_kind = 2;
             I->tpp_rc = cap_s;
             I->tpp_threads = Ts;
-            I->tpp_smem = static_cast<int>(I->to.bytes + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
+            I->tpp_smem = static_cast<int>(tpp_tab_bytes(I) + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
                                            (8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1)) * Ts);
         } else if (rc > 0 && Tr >= 128) {
             I->tpp_kind = 1;
@@ -535,15 +540,21 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     set_ls_cap(I, ready_cap_req);
 }
 
+// table bytes the shared-memory-ready-set TPP kernels stage: the duration-table
+// variant never reads fpay (the last section)
+uint32_t tpp_tab_bytes(const mp_instance *I) {
+    return (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1) ? I->to.fpay : I->to.bytes;
+}
+
 // thread-per-placement shape with a shared-memory ready set of capacity `cap`
 // (local search runs at the group kernel's capacity); threads = 0 if it does not fit
 void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
-    const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;
+    const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - tpp_tab_bytes(I) - 32;
     const long long row = (I->n_ops + 1) / 2;  // nibble-packed row tile
     const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * ((cap + 1) & ~1);  // even slot count
     const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
     *threads = T >= 64 ? T : 0;
-    *smem = static_cast<int>(I->to.bytes + ((row * T + 15) & ~15LL) + (per_lane - row) * T);
+    *smem = static_cast<int>(tpp_tab_bytes(I) + ((row * T + 15) & ~15LL) + (per_lane - row) * T);
 }
 
 // Local search rejects a proposal whose ready set exceeds ls_cap in every kernel,
@@ -573,6 +584,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.colo = I->colo ? 1 : 0;
     a.fastdiv = I->fastdiv ? 1 : 0;
     a.durtab = (I->dur_classes > 0 && !I->durtab_off) ? 1 : 0;
+    a.tpp_stage = I->tpp_kind == 2 ? tpp_tab_bytes(I) : I->to.bytes;
     a.tpp_alt = I->tpp_round1 ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
@@ -661,7 +673,19 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
         }
     }
     const int n_cls = static_cast<int>(h_fcb.empty() ? 0 : upay.size());
-    I->to = make_taboff(n_ops, n_flows, K, n_cls);
+    int h_multi_n = 0, h_src_n = 0;
+    {
+        std::vector<unsigned int> indeg(n_ops, 0u);
+        for (int f = 0; f < n_flows; ++f) {  // the validity test of k_copy_validate
+            const int s0 = prob->flow_src[f], d0 = prob->flow_dst[f];
+            if (s0 >= 0 && s0 < n_ops && d0 >= 0 && d0 < n_ops && s0 != d0) ++indeg[d0];
+        }
+        for (int i = 0; i < n_ops; ++i) {
+            h_multi_n += indeg[i] >= 2;
+            h_src_n += indeg[i] == 0;
+        }
+    }
+    I->to = make_taboff(n_ops, n_flows, K, n_cls, h_multi_n, h_src_n);
 
     auto fail = [&](int code) {
         mp_instance_destroy(I);
