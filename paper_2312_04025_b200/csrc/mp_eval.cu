@@ -1538,32 +1538,40 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     }
     bool done = !alive || ovf;
     double ms = 0.0;
+    // a capacity of exactly four slots (the layered model graphs) is scanned whole,
+    // without the warp-max trip count and loop control
+    const bool cap4 = capA == 4;
     while (__any_sync(kFull, !done)) {
-        const int hbw = (__reduce_max_sync(kFull, done ? 0 : nr) + 1) & ~1;
         // -- scan the ready slots for the minimum (e, -rank, id) key -------------------
         // (one compare-select chain; a two-chain even/odd split measured 1-2 % slower)
         double be = kInf, br = -1.0;
         uint32_t bi = 0xffffffffu;
         int bs = 0;
-        const unsigned long long *p = rE;
-        for (int s = 0; s < hbw; s += 2, p += 2 * T) {
+        auto scan_slot = [&](const unsigned long long *q, int sidx) {
+            const double es = bitsd(q[0]);
+            const double rs = bitsd(q[DR]);
+            const unsigned long long mt = q[DM];
+            const uint32_t m = static_cast<uint32_t>(mt);
+            const double c1 = clk[((m >> 20) & 63u) * T];
+            const double c2 = clk[(m >> 26) * T];
+            double e = c1 > es ? c1 : es;  // NaN es stays NaN: never taken
+            e = c2 > e ? c2 : e;
+            const uint32_t id = (COLO & (e == es)) ? static_cast<uint32_t>(mt >> 32) : (m & MP_NODE_MASK);
+            const bool take = (e < be) | ((e == be) & ((rs > br) | ((rs == br) & (id < bi))));
+            be = take ? e : be;
+            br = take ? rs : br;
+            bi = take ? id : bi;
+            bs = take ? sidx : bs;
+        };
+        if (cap4) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const unsigned long long *q = p + u * T;
-                const double es = bitsd(q[0]);
-                const double rs = bitsd(q[DR]);
-                const unsigned long long mt = q[DM];
-                const uint32_t m = static_cast<uint32_t>(mt);
-                const double c1 = clk[((m >> 20) & 63u) * T];
-                const double c2 = clk[(m >> 26) * T];
-                double e = c1 > es ? c1 : es;  // NaN es stays NaN: never taken
-                e = c2 > e ? c2 : e;
-                const uint32_t id = (COLO & (e == es)) ? static_cast<uint32_t>(mt >> 32) : (m & MP_NODE_MASK);
-                const bool take = (e < be) | ((e == be) & ((rs > br) | ((rs == br) & (id < bi))));
-                be = take ? e : be;
-                br = take ? rs : br;
-                bi = take ? id : bi;
-                bs = take ? s + u : bs;
+            for (int u = 0; u < 4; ++u) scan_slot(rE + u * T, u);
+        } else {
+            const int hbw = (__reduce_max_sync(kFull, done ? 0 : nr) + 1) & ~1;
+            const unsigned long long *p = rE;
+            for (int s = 0; s < hbw; s += 2, p += 2 * T) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) scan_slot(p + u * T, s + u);
             }
         }
         const uint32_t bm = static_cast<uint32_t>(rE[DM + bs * T]);
