@@ -136,6 +136,9 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
 #define MP_TUNE_TPP_ROUND1 16 /* thread-per-placement: the round-1 shared-memory-ready-set evaluator (A/B only) */
 #define MP_TUNE_NO_DURTAB 32 /* thread-per-placement: divide payload / bw at run time instead of
                                reading the flow-duration table (A/B and parity tests) */
+#define MP_TUNE_COST_GLOBAL 64  /* thread-per-placement (duration table): op costs read through L1
+                                  (default: only when that fits 1.5x the lanes, e.g. C3) */
+#define MP_TUNE_COST_SMEM 128   /* ... op costs always staged in shared memory (A/B) */
 #define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernels (used only with
                                automatic G/U) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,

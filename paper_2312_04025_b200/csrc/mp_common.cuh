@@ -40,6 +40,7 @@ struct TabOff {
     uint32_t fdur;      // f64 [n_cls*K*K]  flow-duration table: payload class c, pair (a, b) at c*K*K + a*K + b
                         //                  = (double)payload_c / bw[a][b] (IEEE, solver.py:93-96); 0 on the diagonal
     uint32_t fcb;       // u32 [n_flows]    duration-table base c*K*K of each flow (by flow index)
+    uint32_t s_rec8;    // u64 [n_flows]    the first word of s_rec (duration-table kernels: no payload)
     uint32_t fpay;      // f64 [n_flows]    payload by flow index (durations recomputed at commit by the
                         //                  division variants; last, so the table variant stages [0, fpay))
     uint32_t bytes;     // total, multiple of 16
@@ -73,6 +74,7 @@ struct EvalArgs {
     int colo;                     // skip co-located flows (exact when all durations > 0)
     int fastdiv;                  // payload/bw via verified reciprocal + one Markstein correction
     int durtab;                   // flow durations read from the to.fdur table (few distinct payloads)
+    int cost_global;              // TPP duration-table kernel: op costs read from global memory (L1)
     uint32_t tpp_stage;           // TPP kernels: table bytes staged into shared memory (to.fpay with the
                                   // duration table, else to.bytes); the row tile starts there
 

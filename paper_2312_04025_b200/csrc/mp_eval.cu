@@ -770,6 +770,7 @@ struct TppView {
     const double *T_fpay;              // payload by flow index
     const double *T_fdur;              // flow-duration table (EvalArgs::durtab)
     const uint32_t *T_fcb;             // its base by flow index
+    const unsigned long long *T_rec8;  // slot records without the payload (duration-table kernels)
 };
 
 // nib: the row tile holds two device indices per byte (shared-memory ready-set
@@ -816,6 +817,7 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.T_fpay = tab<double>(tb, a.to.fpay);
     v.T_fdur = tab<double>(tb, a.to.fdur);
     v.T_fcb = tab<uint32_t>(tb, a.to.fcb);
+    v.T_rec8 = tab<unsigned long long>(tb, a.to.s_rec8);
     return v;
 }
 
@@ -1415,7 +1417,7 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
 //     64-bit word, so a consumer update is one 8-byte and one 16-byte round trip.
 // Global per-lane state (lane-interleaved [index][L], tpp_state_bytes): rank f64
 // [n_ops], est f64 [n_multi], tie | npred << 32 u64 [n_multi].
-template <bool COLO, bool TAB>
+template <bool COLO, bool TAB, bool GC = false>
 __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs &a, bool live, bool bad, int cap) {
     const int T = v.T, n_ops = v.n_ops, K = v.K;
     const unsigned char *__restrict__ rowl = v.rowt + v.tid;  // op x: rowl[(x >> 1) * T], nibble (x & 1)
@@ -1434,7 +1436,11 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     auto gm = [&](unsigned k) -> double2 * {
         return reinterpret_cast<double2 *>(g_m + static_cast<unsigned long long>(k * L16));
     };
-    const double *__restrict__ T_cost = v.T_cost;
+    // GC: op costs from global memory through L1 (not staged: wide graphs), per-lane state
+    // loads bypass L1 so the costs stay resident there
+    const double *__restrict__ T_cost = GC ? reinterpret_cast<const double *>(a.blob + a.to.cost) : v.T_cost;
+    auto cost = [&](int x) -> double { return GC ? __ldg(T_cost + x) : T_cost[x]; };
+    const unsigned long long *__restrict__ T_rec8 = v.T_rec8;  // TAB: {dst | base << 20, node id}
     const long long *__restrict__ T_mem = v.T_mem;
     const long long *__restrict__ T_cap = v.T_cap;
     const double *__restrict__ T_bw = v.T_bw;
@@ -1484,22 +1490,21 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         double best = 0.0;
         const int qe = static_cast<int>(T_out_beg[i + 1]);
         for (int q = static_cast<int>(T_out_beg[i]); q < qe; ++q) {
-            const double2 rec = T_rec[q];
-            const uint32_t lo = static_cast<uint32_t>(dbits(rec.x));
+            const uint32_t lo = TAB ? static_cast<uint32_t>(T_rec8[q]) : static_cast<uint32_t>(dbits(T_rec[q].x));
             const int j = static_cast<int>(lo & MP_NODE_MASK);
             const int dj = dev(j);
-            const double rj = *grank(j);
+            const double rj = GC ? __ldcg(grank(j)) : *grank(j);
             double fr = rj;
             if constexpr (TAB) {
                 const double du = T_fdur[(lo >> MP_NODE_BITS) + d * K + dj];
                 fr = dj != d ? du + rj : rj;
             } else if (dj != d) {  // warp-divergent only in timing: both sides are short
                 const int bi = d * K + dj;
-                fr = div_bw(rec.y, T_bw[bi], T_rbw[bi], fast) + rj;
+                fr = div_bw(T_rec[q].y, T_bw[bi], T_rbw[bi], fast) + rj;
             }
             best = fr > best ? fr : best;
         }
-        *grank(i) = T_cost[i * K + d] + best;
+        *grank(i) = cost(i * K + d) + best;
     }
 
     // ---- 4. dispatch state (solver.py:109-116) -----------------------------------------
@@ -1531,7 +1536,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     if (alive) {
         for (int t = 0; t < a.n_src; ++t) {
             const int i = static_cast<int>(T_srcs[t]);
-            insert(true, 0ULL, dbits(*grank(i)),
+            insert(true, 0ULL, dbits(GC ? __ldcg(grank(i)) : *grank(i)),
                    static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev(i)) << 20) | (RZ << 26),
                    static_cast<uint32_t>(i));
         }
@@ -1599,8 +1604,16 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
             for (int u = 0; u < SU; ++u) {
                 const int t = t0 + u;
                 const bool act = t < cnt;
-                const double2 rec = T_rec[(act & isop) ? ob + t : 0];
-                const unsigned long long rb = dbits(rec.x);
+                const int qq = (act & isop) ? ob + t : 0;
+                unsigned long long rb;
+                double ry = 0.0;
+                if constexpr (TAB) {
+                    rb = T_rec8[qq];
+                } else {
+                    const double2 rec = T_rec[qq];
+                    rb = dbits(rec.x);
+                    ry = rec.y;
+                }
                 const int j = static_cast<int>(isop ? (static_cast<uint32_t>(rb) & MP_NODE_MASK) : jflow);
                 j_[u] = j;
                 dj_[u] = dev(j);
@@ -1608,17 +1621,17 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 if constexpr (TAB) {
                     cb_[u] = static_cast<uint32_t>(rb) >> MP_NODE_BITS;
                 } else {
-                    pay_[u] = rec.y;
+                    pay_[u] = ry;
                 }
                 act_[u] = act;
-                rj_[u] = *grank(j);
+                rj_[u] = GC ? __ldcg(grank(j)) : *grank(j);
                 const uint32_t k = T_mi[j];
                 k_[u] = k;
                 const bool op_upd = act & !(isop & !(COLO & (dj_[u] == d)));
                 tn_[u] = 1ULL << 32;
                 cur_[u] = 0.0;
                 if (op_upd & (k != MP_NONE)) {
-                    const double2 ms2 = *gm(k);
+                    const double2 ms2 = GC ? __ldcg(gm(k)) : *gm(k);
                     cur_[u] = ms2.x;
                     tn_[u] = dbits(ms2.y);
                 }
@@ -1629,7 +1642,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         // co-located flow dispatched as a node (colo off)
         double bd = 0.0;
         if (!done && node < n_ops) {
-            bd = T_cost[node * K + d];
+            bd = cost(node * K + d);
         } else if (!done && r1 != RZ) {
             const int bi2 = (d - K) * K + (static_cast<int>(r2) - 2 * K);
             if constexpr (TAB) {
@@ -1837,6 +1850,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
         const bool bad = tpp_load_row<true>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
         const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, bad, a.rcap)
                             : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, bad, a.rcap)
+                            : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, bad, a.rcap)
                                        : tpp2_eval<COLO, false>(v, a, live, bad, a.rcap);
         if (live) {
             const long long o = grow - a.out_base;
@@ -1885,6 +1899,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
         tpp_load_row<true>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
         const TppResult r0 = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
                              : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
+                             : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, false, a.rcap)
                                         : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
         double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
@@ -1897,6 +1912,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
             if (live) *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (nd << sh));
             const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
                                 : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
+                                : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, false, a.rcap)
                                            : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
@@ -2114,7 +2130,8 @@ cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, c
     static bool attr = false;
     if (!attr) {
         for (EvalFn f : {mp_tpps_kernel<true, 0>, mp_tpps_kernel<false, 0>, mp_tpps_kernel<true, 1>,
-                         mp_tpps_kernel<false, 1>, mp_tpps_kernel<true, 2>, mp_tpps_kernel<false, 2>}) {
+                         mp_tpps_kernel<false, 1>, mp_tpps_kernel<true, 2>, mp_tpps_kernel<false, 2>,
+                         mp_tpps_kernel<true, 3>, mp_tpps_kernel<false, 3>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
@@ -2122,6 +2139,7 @@ cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, c
         attr = true;
     }
     EvalFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_kernel<true, 1> : mp_tpps_kernel<false, 1>)
+               : a.cost_global ? (a.colo ? mp_tpps_kernel<true, 3> : mp_tpps_kernel<false, 3>)
                : a.durtab    ? (a.colo ? mp_tpps_kernel<true, 2> : mp_tpps_kernel<false, 2>)
                              : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a);
@@ -2133,7 +2151,8 @@ cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a
     static bool attr = false;
     if (!attr) {
         for (LsFn f : {mp_tpps_ls_kernel<true, 0>, mp_tpps_ls_kernel<false, 0>, mp_tpps_ls_kernel<true, 1>,
-                       mp_tpps_ls_kernel<false, 1>, mp_tpps_ls_kernel<true, 2>, mp_tpps_ls_kernel<false, 2>}) {
+                       mp_tpps_ls_kernel<false, 1>, mp_tpps_ls_kernel<true, 2>, mp_tpps_ls_kernel<false, 2>,
+                       mp_tpps_ls_kernel<true, 3>, mp_tpps_ls_kernel<false, 3>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
@@ -2141,6 +2160,7 @@ cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a
         attr = true;
     }
     LsFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_ls_kernel<true, 1> : mp_tpps_ls_kernel<false, 1>)
+             : a.cost_global ? (a.colo ? mp_tpps_ls_kernel<true, 3> : mp_tpps_ls_kernel<false, 3>)
              : a.durtab    ? (a.colo ? mp_tpps_ls_kernel<true, 2> : mp_tpps_ls_kernel<false, 2>)
                            : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>);
     f<<<ctas, threads, smem, s>>>(a, ls);

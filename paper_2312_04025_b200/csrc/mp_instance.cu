@@ -132,6 +132,7 @@ __global__ void k_slots(int n_ops, int n_flows, const unsigned int *sorted_f, co
         const unsigned long long w = static_cast<unsigned long long>(lo) |
                                      (static_cast<unsigned long long>(static_cast<uint32_t>(n_ops) + f) << 32);
         reinterpret_cast<double2 *>(blob + to.s_rec)[q] = make_double2(__longlong_as_double(static_cast<long long>(w)), pay_d[f]);
+        if (durtab) reinterpret_cast<unsigned long long *>(blob + to.s_rec8)[q] = w;
     }
 }
 
@@ -296,22 +297,25 @@ TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls, int n_multi, int n_
         o = align16(o + std::max<uint64_t>(bytes, 16));
         return at;
     };
-    t.cost = take(8ULL * n_ops * K);
+    // staged prefixes of the duration-table TPP kernels: [0, cost) with costs read through
+    // L1 (wide graphs), [0, s_rec) with costs in shared memory; the rest serves the other kernels
     t.mem = take(8ULL * n_ops);
-    t.bw = take(8ULL * K * K);
-    t.rbw = take(8ULL * K * K);
     t.cap = take(8ULL * K);
     t.out_beg = take(4ULL * (n_ops + 1));
-    t.s_rec = take(16ULL * n_flows);
     t.fdst = take(4ULL * n_flows);
     t.mi = take(4ULL * n_ops);
     t.m_op = take(4ULL * n_multi);
     t.m_deg = take(4ULL * n_multi);
     t.lvl_ops = take(4ULL * n_ops);
-    t.lvl_beg = take(4ULL * (n_ops + 1));
     t.srcs = take(4ULL * n_src);
     t.fdur = take(8ULL * n_cls * K * K);
     t.fcb = take(n_cls > 0 ? 4ULL * n_flows : 0);
+    t.s_rec8 = take(n_cls > 0 ? 8ULL * n_flows : 0);
+    t.cost = take(8ULL * n_ops * K);
+    t.s_rec = take(16ULL * n_flows);
+    t.bw = take(8ULL * K * K);
+    t.rbw = take(8ULL * K * K);
+    t.lvl_beg = take(4ULL * (n_ops + 1));
     t.fpay = take(8ULL * n_flows);
     t.bytes = static_cast<uint32_t>(o);
     return t;
@@ -347,6 +351,8 @@ struct mp_instance {
     int slow_div_pairs = 0;
     int dur_classes = 0;   // distinct payloads in the flow-duration table (0: durations divided at run time)
     bool durtab_off = false;  // MP_TUNE_NO_DURTAB
+    bool cost_global = false; // duration-table TPP kernel reads op costs through L1 (chosen by lanes)
+    int cost_mode = 0;        // 0 automatic, 1 MP_TUNE_COST_GLOBAL, 2 MP_TUNE_COST_SMEM
     int sms = 0;
     int rcap_target = 32;
     int peak_probe = -1;   // largest ready set seen on the calibration probe (-1 = not run)
@@ -505,6 +511,18 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     // tables + per-lane row and clocks (+ ready entries) in shared memory
     I->tpp_rc = 0;
     I->tpp_kind = 0;
+    // Duration-table TPP: op costs stay in shared memory unless reading them through L1
+    // lets 1.5x the lanes fit (wide graphs such as C3, whose tables would leave < 128 lanes)
+    I->cost_global = false;
+    if (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1 && I->cost_mode != 2) {
+        const int cap_s = ready_cap_req > 0 ? std::max(1, std::min(I->ready_bound, I->rcap_target))
+                                            : std::min(I->ready_bound, std::max(4, I->peak_probe > 0 ? I->peak_probe : 4));
+        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1);
+        const long long t_s = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.s_rec - 32) / lane_s;
+        const long long t_g = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.cost - 32) / lane_s;
+        I->cost_global = I->cost_mode == 1 || (2 * std::min<long long>(t_g, MP_TPP_MAX_THREADS) >=
+                                               3 * std::min<long long>(t_s, MP_TPP_MAX_THREADS));
+    }
     if (I->tpp_allowed && G_req == 0 && U_req == 0 && I->peak_probe >= 0) {
         const int want = ready_cap_req > 0 ? rcap : std::max(1, std::min(I->ready_bound, I->peak_probe));
         const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.bytes - 32;  // register variant
@@ -543,7 +561,8 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
 // table bytes the shared-memory-ready-set TPP kernels stage: the duration-table
 // variant never reads fpay (the last section)
 uint32_t tpp_tab_bytes(const mp_instance *I) {
-    return (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1) ? I->to.fpay : I->to.bytes;
+    if (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1) return I->cost_global ? I->to.cost : I->to.s_rec;
+    return I->to.bytes;
 }
 
 // thread-per-placement shape with a shared-memory ready set of capacity `cap`
@@ -585,6 +604,7 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.fastdiv = I->fastdiv ? 1 : 0;
     a.durtab = (I->dur_classes > 0 && !I->durtab_off) ? 1 : 0;
     a.tpp_stage = I->tpp_kind == 2 ? tpp_tab_bytes(I) : I->to.bytes;
+    a.cost_global = (a.durtab && I->cost_global && I->tpp_kind == 2) ? 1 : 0;
     a.tpp_alt = I->tpp_round1 ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
@@ -1011,6 +1031,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->tpp_round1 = (flags & MP_TUNE_TPP_ROUND1) != 0;
     I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
     I->durtab_off = (flags & MP_TUNE_NO_DURTAB) != 0;
+    I->cost_mode = (flags & MP_TUNE_COST_GLOBAL) ? 1 : ((flags & MP_TUNE_COST_SMEM) ? 2 : 0);
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--offchip", action="store_true")
     ap.add_argument("--round1", action="store_true", help="the round-1 TPP evaluator (A/B)")
     ap.add_argument("--no-durtab", action="store_true", help="divide flow durations at run time (A/B)")
+    ap.add_argument("--costs", default="auto", choices=("auto", "global", "smem"), help="TPP op-cost placement (A/B)")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     args = ap.parse_args()
@@ -56,7 +57,7 @@ def main():
         G, U = (int(x) for x in (spec.split(":") + ["0"])[:2])
         inst.tune(G, args.ctas_per_sm, ready_cap=args.rcap, colo=not args.no_colo, lanes_used=U, tpp=not args.no_tpp,
                   tpp_registers=args.tpp_reg, offchip=args.offchip, tpp_round1=args.round1,
-                  durtab=not args.no_durtab)
+                  durtab=not args.no_durtab, costs=args.costs)
         info = inst.info()
         best = C.c_int64()
         bms = C.c_double()
