@@ -139,6 +139,8 @@ int32_t mp_instance_info_get(const mp_instance *inst, mp_instance_info *info);
 #define MP_TUNE_COST_GLOBAL 64  /* thread-per-placement (duration table): op costs read through L1
                                   (default: only when that fits 1.5x the lanes, e.g. C3) */
 #define MP_TUNE_COST_SMEM 128   /* ... op costs always staged in shared memory (A/B) */
+#define MP_TUNE_ROW3 256       /* thread-per-placement: 3-bit row tile whenever K <= 8 (default: only
+                                  where it fits more lanes than nibbles) */
 #define MP_TUNE_NO_TPP  2   /* do not use the thread-per-placement kernels (used only with
                                automatic G/U) */
 int32_t mp_instance_tune(mp_instance *inst, int32_t group_lanes, int32_t lanes_used, int32_t ctas_per_sm,

@@ -75,6 +75,8 @@ struct EvalArgs {
     int fastdiv;                  // payload/bw via verified reciprocal + one Markstein correction
     int durtab;                   // flow durations read from the to.fdur table (few distinct payloads)
     int cost_global;              // TPP duration-table kernel: op costs read from global memory (L1)
+    int tpp_rb;                   // TPP row tile: 8 bits per op (register variant), 4 (nibbles), 3 (K <= 8)
+    int tpp_nclk;                 // TPP clock slots per lane: 3K (round-2 evaluator with colo), else 3K + 2
     uint32_t tpp_stage;           // TPP kernels: table bytes staged into shared memory (to.fpay with the
                                   // duration table, else to.bytes); the row tile starts there
 

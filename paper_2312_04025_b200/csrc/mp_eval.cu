@@ -775,6 +775,12 @@ struct TppView {
 
 // nib: the row tile holds two device indices per byte (shared-memory ready-set
 // variant, K <= 16), (n_ops + 1) / 2 bytes per lane
+// Row tile per lane by a.tpp_rb: 8 = one byte per op, 4 = two ops per byte (low nibble =
+// even op), 3 = 21 ops per 64-bit word (K <= 8); see tpp_row_bytes.
+__host__ __device__ __forceinline__ size_t tpp_row_bytes_dev(int rb, int n_ops) {
+    return rb == 3 ? 8ULL * ((n_ops + 20) / 21) : (rb == 4 ? static_cast<size_t>((n_ops + 1) / 2) : static_cast<size_t>(n_ops));
+}
+
 __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm, bool nib = false) {
     TppView v;
     v.T = blockDim.x;
@@ -782,7 +788,7 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.n_ops = a.n_ops;
     v.K = a.K;
     v.rowt = sm + a.tpp_stage;
-    const size_t row_bytes = nib ? static_cast<size_t>((a.n_ops + 1) / 2) : static_cast<size_t>(a.n_ops);
+    const size_t row_bytes = tpp_row_bytes_dev(nib ? a.tpp_rb : 8, a.n_ops);
     v.clk = reinterpret_cast<double *>(sm + a.tpp_stage + ((row_bytes * v.T + 15) & ~static_cast<size_t>(15)));
     v.ld = reinterpret_cast<unsigned long long *>(v.clk);
     v.L = a.lane_stride;
@@ -811,7 +817,7 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
     v.WS = v.RZ + 1;
     // an even number of ready slots per lane (tpp2_eval scans two per iteration)
     const size_t rdy = static_cast<size_t>((a.rcap + 1) & ~1) * v.T;
-    v.rE = reinterpret_cast<unsigned long long *>(v.clk + static_cast<size_t>(3 * a.K + 2) * v.T);
+    v.rE = reinterpret_cast<unsigned long long *>(v.clk + static_cast<size_t>(a.tpp_nclk) * v.T);
     v.rR = v.rE + rdy;
     v.rM = v.rR + rdy;
     v.T_fpay = tab<double>(tb, a.to.fpay);
@@ -824,11 +830,14 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
 // Load one placement row (global byte offset `start`) into this lane's column of
 // the row tile with 16-byte L2 loads; returns true if it names a device >= K.
 // NIB: pack two device indices per byte (low nibble = even op).
-template <bool NIB = false>
+// R3: 21 three-bit device indices per 64-bit word, words lane-interleaved [w][T].
+template <bool NIB = false, bool R3 = false>
 __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *rows, long long rows_bytes,
                                              long long start, bool live) {
     bool bad = false;
     const int n_ops = v.n_ops, T = v.T, tid = v.tid;
+    unsigned long long *row64 = reinterpret_cast<unsigned long long *>(v.rowt) + tid;
+    unsigned long long acc = 0;
     const long long a0 = start & ~15LL;
     const long long a1 = (start + n_ops + 15) & ~15LL;
     const int chunks = live ? static_cast<int>((a1 - a0) >> 4) : 0;
@@ -850,7 +859,15 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
             if (pos >= 0 && pos < n_ops) {
                 const unsigned char d = static_cast<unsigned char>(w4[b >> 2] >> (8 * (b & 3)));
                 bad |= d >= v.K;
-                if constexpr (NIB) {
+                if constexpr (R3) {
+                    const int p = static_cast<int>(pos);
+                    const int w = p / 21, r = p - 21 * w;
+                    acc |= static_cast<unsigned long long>(d & 7u) << (3 * r);
+                    if (r == 20 || p == n_ops - 1) {
+                        row64[w * T] = acc;
+                        acc = 0;
+                    }
+                } else if constexpr (NIB) {
                     unsigned char *cell = &v.rowt[(pos >> 1) * T + tid];
                     *cell = (pos & 1) ? static_cast<unsigned char>((*cell & 0x0Fu) | ((d & 15u) << 4))
                                       : static_cast<unsigned char>(d & 15u);
@@ -861,10 +878,39 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
         }
     }
     if (!live || bad) {  // keep the lockstep passes in bounds
-        const int nb = NIB ? (n_ops + 1) / 2 : n_ops;
-        for (int i = 0; i < nb; ++i) v.rowt[i * T + tid] = 0;
+        if constexpr (R3) {
+            for (int i = 0; i < (n_ops + 20) / 21; ++i) row64[i * T] = 0ULL;
+        } else {
+            const int nb = NIB ? (n_ops + 1) / 2 : n_ops;
+            for (int i = 0; i < nb; ++i) v.rowt[i * T + tid] = 0;
+        }
     }
     return bad;
+}
+
+// device index of op i in this lane's column of a nibble (R3 = false) or 3-bit row tile
+template <bool R3>
+__device__ __forceinline__ int tpp_row_get(const TppView &v, int i) {
+    if constexpr (R3) {
+        const int w = i / 21;
+        return static_cast<int>((reinterpret_cast<const unsigned long long *>(v.rowt)[w * v.T + v.tid] >>
+                                 (3 * (i - 21 * w))) & 7ULL);
+    } else {
+        return (v.rowt[(i >> 1) * v.T + v.tid] >> ((i & 1) << 2)) & 15;
+    }
+}
+
+template <bool R3>
+__device__ __forceinline__ void tpp_row_set(const TppView &v, int i, int d) {
+    if constexpr (R3) {
+        const int w = i / 21, sh = 3 * (i - 21 * w);
+        unsigned long long *c = reinterpret_cast<unsigned long long *>(v.rowt) + w * v.T + v.tid;
+        *c = (*c & ~(7ULL << sh)) | (static_cast<unsigned long long>(d) << sh);
+    } else {
+        unsigned char *cell = &v.rowt[(i >> 1) * v.T + v.tid];
+        const int sh = (i & 1) << 2;
+        *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (d << sh));
+    }
 }
 
 struct TppResult {
@@ -1417,7 +1463,9 @@ __device__ __forceinline__ TppResult tpps_eval(const TppView &v, const EvalArgs 
 //     64-bit word, so a consumer update is one 8-byte and one 16-byte round trip.
 // Global per-lane state (lane-interleaved [index][L], tpp_state_bytes): rank f64
 // [n_ops], est f64 [n_multi], tie | npred << 32 u64 [n_multi].
-template <bool COLO, bool TAB, bool GC = false>
+// R3: 3-bit row tile.  COLO: 3K clock slots (an op entry reads its device clock twice, so
+// no zero slot is needed, and no co-located flow is ever dispatched, so no sink either).
+template <bool COLO, bool TAB, bool GC = false, bool R3 = false>
 __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs &a, bool live, bool bad, int cap) {
     const int T = v.T, n_ops = v.n_ops, K = v.K;
     const unsigned char *__restrict__ rowl = v.rowt + v.tid;  // op x: rowl[(x >> 1) * T], nibble (x & 1)
@@ -1461,7 +1509,17 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     const int capA = (a.rcap + 1) & ~1;
     unsigned long long *__restrict__ rE = v.rE + v.tid;  // slot s: rE[s * T]; rank / meta at fixed offsets
     const size_t DR = static_cast<size_t>(v.rR - v.rE), DM = static_cast<size_t>(v.rM - v.rE);
-    auto dev = [&](int x) -> int { return (rowl[(x >> 1) * T] >> ((x & 1) << 2)) & 15; };
+    const unsigned long long *__restrict__ rowl64 = reinterpret_cast<const unsigned long long *>(v.rowt) + v.tid;
+    auto dev = [&](int x) -> int {
+        if constexpr (R3) {
+            const int w = static_cast<int>(__umulhi(static_cast<unsigned>(x), 204522253u));  // x / 21
+            return static_cast<int>((rowl64[w * T] >> (3 * (x - 21 * w))) & 7ULL);
+        } else {
+            return (rowl[(x >> 1) * T] >> ((x & 1) << 2)) & 15;
+        }
+    };
+    // second clock slot of an op entry: none (RZ) without colo, the op's own clock with it
+    auto op_r2 = [&](uint32_t d) -> uint32_t { return COLO ? d : RZ; };
     TppResult r;
     // ---- 1. memory feasibility (solver.py:82-87) ------------------------------------
     int status = bad ? MP_ROW_BAD_DEVICE : MP_ROW_OK;
@@ -1511,9 +1569,10 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     for (int k = 0; k < a.n_multi; ++k)
         *gm(k) = make_double2(0.0, bitsd(static_cast<unsigned long long>(T_mop[k]) |
                                          (static_cast<unsigned long long>(T_mdeg[k]) << 32)));
-    for (int k = 0; k <= static_cast<int>(WS); ++k) clk[k * T] = 0.0;
+    for (int k = 0; k < a.tpp_nclk; ++k) clk[k * T] = 0.0;
     const unsigned long long NAN_BITS = 0xfff8000000000000ULL;
-    const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (RZ << 20) | (RZ << 26));
+    const uint32_t SZ = COLO ? 0u : RZ;  // vacated slots read any clock (their NaN est is never taken)
+    const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (SZ << 20) | (SZ << 26));
     for (int s = 0; s < capA; ++s) {
         rE[s * T] = NAN_BITS;
         rE[DM + s * T] = SENT_M;
@@ -1537,7 +1596,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         for (int t = 0; t < a.n_src; ++t) {
             const int i = static_cast<int>(T_srcs[t]);
             insert(true, 0ULL, dbits(GC ? __ldcg(grank(i)) : *grank(i)),
-                   static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev(i)) << 20) | (RZ << 26),
+                   static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev(i)) << 20) | (op_r2(dev(i)) << 26),
                    static_cast<uint32_t>(i));
         }
     }
@@ -1668,8 +1727,13 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         // -- commit (solver.py:130-138) ------------------------------------------------
         const double end = be + bd;
         if (!done) {
-            clk[(r1 == RZ ? WS : r1) * T] = end;
-            clk[(r2 == RZ ? WS : r2) * T] = end;
+            if constexpr (COLO) {  // an op writes its clock twice; a flow its two channel clocks
+                clk[r1 * T] = end;
+                clk[r2 * T] = end;
+            } else {
+                clk[(r1 == RZ ? WS : r1) * T] = end;
+                clk[(r2 == RZ ? WS : r2) * T] = end;
+            }
         }
         ms = (!done & (node < n_ops) & (end > ms)) ? end : ms;
         // -- successors (solver.py:140-145): op -> its out-flows, flow -> its consumer
@@ -1711,7 +1775,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                                                         (static_cast<unsigned long long>(np) << 32)));
                 const bool op_ins = op_upd & (!multi | (np == 0u));
                 insert(flow_ins | op_ins, dbits(flow_ins ? end : ej), dbits(flow_ins ? fdur + rj : rj),
-                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
+                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (op_r2(dj) << 26)),
                        flow_ins ? pid : (multi ? tie_new : tj));
             }
         }
@@ -1822,7 +1886,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpp_ls_kernel(const 
 }
 
 // ---- thread per placement, ready set in shared memory ----------------------------------
-template <bool COLO, int VAR>
+template <bool COLO, int VAR, bool R3 = false>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t s_bar;
@@ -1847,11 +1911,11 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
         const bool live = p < static_cast<unsigned long long>(n_rows);
         const long long lrow = live ? (a.row_list ? a.row_idx[p] - a.row_base : static_cast<long long>(p)) : 0;
         const long long grow = a.row_base + lrow;
-        const bool bad = tpp_load_row<true>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
+        const bool bad = tpp_load_row<true, R3>(v, a.rows, a.rows_bytes, lrow * a.n_ops, live);
         const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, bad, a.rcap)
-                            : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, bad, a.rcap)
-                            : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, bad, a.rcap)
-                                       : tpp2_eval<COLO, false>(v, a, live, bad, a.rcap);
+                            : VAR == 2 ? tpp2_eval<COLO, true, false, R3>(v, a, live, bad, a.rcap)
+                            : VAR == 3 ? tpp2_eval<COLO, true, true, R3>(v, a, live, bad, a.rcap)
+                                       : tpp2_eval<COLO, false, false, R3>(v, a, live, bad, a.rcap);
         if (live) {
             const long long o = grow - a.out_base;
             if (r.ovf) {
@@ -1878,7 +1942,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_kernel(const __
 // K5 on the thread-per-placement layout (shared-memory ready set): one lane per chain, the chain's row in
 // its tile column.  Same proposals, acceptance rule and ready capacity (`a.rcap`,
 // the group kernel's) as mp_ls_kernel, so results do not depend on the kernel.
-template <bool COLO, int VAR>
+template <bool COLO, int VAR, bool R3 = false>
 __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const __grid_constant__ EvalArgs a,
                                                                          const __grid_constant__ LsArgs ls) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1886,7 +1950,7 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
     const int lane = threadIdx.x & 31;
     stage_tables(sm, a, &s_bar, a.tpp_stage);
     const TppView v = tpp_view(a, sm, true);
-    const int n = a.n_ops, K = a.K, T = v.T, tid = v.tid;
+    const int n = a.n_ops, K = a.K;
     for (;;) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(a.next, 32ULL);
@@ -1896,33 +1960,31 @@ __global__ void __launch_bounds__(MP_TPP_MAX_THREADS, 1) mp_tpps_ls_kernel(const
         const bool live = c < static_cast<unsigned long long>(ls.n_chains);
         const unsigned long long gc = c + static_cast<unsigned long long>(ls.chain_base);
         const long long srow = live ? static_cast<long long>(gc % static_cast<unsigned long long>(ls.n_seed)) : 0;
-        tpp_load_row<true>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
+        tpp_load_row<true, R3>(v, ls.seed_rows, static_cast<long long>(ls.n_seed) * n, srow * n, live);
         const TppResult r0 = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
-                             : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
-                             : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, false, a.rcap)
-                                        : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
+                             : VAR == 2 ? tpp2_eval<COLO, true, false, R3>(v, a, live, false, a.rcap)
+                             : VAR == 3 ? tpp2_eval<COLO, true, true, R3>(v, a, live, false, a.rcap)
+                                        : tpp2_eval<COLO, false, false, R3>(v, a, live, false, a.rcap);
         double cur_ms = (!r0.ovf && r0.alive) ? r0.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
             const int i = static_cast<int>((h & 0xffffffffULL) % static_cast<unsigned long long>(n));
-            unsigned char *cell = &v.rowt[(i >> 1) * T + tid];
-            const int sh = (i & 1) << 2;
-            const int old = (*cell >> sh) & 15;
+            const int old = tpp_row_get<R3>(v, i);
             const int nd = (old + 1 + static_cast<int>((h >> 32) % static_cast<unsigned long long>(K - 1))) % K;
-            if (live) *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (nd << sh));
+            if (live) tpp_row_set<R3>(v, i, nd);
             const TppResult r = VAR == 1   ? tpps_eval<COLO>(v, a, live, false, a.rcap)
-                                : VAR == 2 ? tpp2_eval<COLO, true>(v, a, live, false, a.rcap)
-                                : VAR == 3 ? tpp2_eval<COLO, true, true>(v, a, live, false, a.rcap)
-                                           : tpp2_eval<COLO, false>(v, a, live, false, a.rcap);
+                                : VAR == 2 ? tpp2_eval<COLO, true, false, R3>(v, a, live, false, a.rcap)
+                                : VAR == 3 ? tpp2_eval<COLO, true, true, R3>(v, a, live, false, a.rcap)
+                                           : tpp2_eval<COLO, false, false, R3>(v, a, live, false, a.rcap);
             const double ms = (!r.ovf && r.alive) ? r.ms : kInf;
             if (!r.ovf && ms <= cur_ms) {
                 cur_ms = ms;
             } else if (live) {
-                *cell = static_cast<unsigned char>((*cell & ~(15 << sh)) | (old << sh));
+                tpp_row_set<R3>(v, i, old);
             }
         }
         if (live) {
-            for (int i = 0; i < n; ++i) ls.chain_rows[c * n + i] = (v.rowt[(i >> 1) * T + tid] >> ((i & 1) << 2)) & 15;
+            for (int i = 0; i < n; ++i) ls.chain_rows[c * n + i] = static_cast<uint8_t>(tpp_row_get<R3>(v, i));
             ls.chain_ms[c] = cur_ms;
         }
         __syncwarp();
@@ -2131,17 +2193,26 @@ cudaError_t mp_launch_tpps(int threads, int ctas, int smem, const EvalArgs &a, c
     if (!attr) {
         for (EvalFn f : {mp_tpps_kernel<true, 0>, mp_tpps_kernel<false, 0>, mp_tpps_kernel<true, 1>,
                          mp_tpps_kernel<false, 1>, mp_tpps_kernel<true, 2>, mp_tpps_kernel<false, 2>,
-                         mp_tpps_kernel<true, 3>, mp_tpps_kernel<false, 3>}) {
+                         mp_tpps_kernel<true, 3>, mp_tpps_kernel<false, 3>, mp_tpps_kernel<true, 0, true>,
+                         mp_tpps_kernel<false, 0, true>, mp_tpps_kernel<true, 2, true>,
+                         mp_tpps_kernel<false, 2, true>, mp_tpps_kernel<true, 3, true>,
+                         mp_tpps_kernel<false, 3, true>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
+    const bool r3 = a.tpp_rb == 3;
     EvalFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_kernel<true, 1> : mp_tpps_kernel<false, 1>)
-               : a.cost_global ? (a.colo ? mp_tpps_kernel<true, 3> : mp_tpps_kernel<false, 3>)
-               : a.durtab    ? (a.colo ? mp_tpps_kernel<true, 2> : mp_tpps_kernel<false, 2>)
-                             : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>);
+               : a.cost_global
+                   ? (r3 ? (a.colo ? mp_tpps_kernel<true, 3, true> : mp_tpps_kernel<false, 3, true>)
+                         : (a.colo ? mp_tpps_kernel<true, 3> : mp_tpps_kernel<false, 3>))
+               : a.durtab
+                   ? (r3 ? (a.colo ? mp_tpps_kernel<true, 2, true> : mp_tpps_kernel<false, 2, true>)
+                         : (a.colo ? mp_tpps_kernel<true, 2> : mp_tpps_kernel<false, 2>))
+                   : (r3 ? (a.colo ? mp_tpps_kernel<true, 0, true> : mp_tpps_kernel<false, 0, true>)
+                         : (a.colo ? mp_tpps_kernel<true, 0> : mp_tpps_kernel<false, 0>));
     f<<<ctas, threads, smem, s>>>(a);
     ++g_mp_launches;
     return cudaGetLastError();
@@ -2152,17 +2223,26 @@ cudaError_t mp_launch_tpps_ls(int threads, int ctas, int smem, const EvalArgs &a
     if (!attr) {
         for (LsFn f : {mp_tpps_ls_kernel<true, 0>, mp_tpps_ls_kernel<false, 0>, mp_tpps_ls_kernel<true, 1>,
                        mp_tpps_ls_kernel<false, 1>, mp_tpps_ls_kernel<true, 2>, mp_tpps_ls_kernel<false, 2>,
-                       mp_tpps_ls_kernel<true, 3>, mp_tpps_ls_kernel<false, 3>}) {
+                       mp_tpps_ls_kernel<true, 3>, mp_tpps_ls_kernel<false, 3>, mp_tpps_ls_kernel<true, 0, true>,
+                       mp_tpps_ls_kernel<false, 0, true>, mp_tpps_ls_kernel<true, 2, true>,
+                       mp_tpps_ls_kernel<false, 2, true>, mp_tpps_ls_kernel<true, 3, true>,
+                       mp_tpps_ls_kernel<false, 3, true>}) {
             cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(f),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, MP_TPP_SMEM_MAX);
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
+    const bool r3 = a.tpp_rb == 3;
     LsFn f = a.tpp_alt == 1 ? (a.colo ? mp_tpps_ls_kernel<true, 1> : mp_tpps_ls_kernel<false, 1>)
-             : a.cost_global ? (a.colo ? mp_tpps_ls_kernel<true, 3> : mp_tpps_ls_kernel<false, 3>)
-             : a.durtab    ? (a.colo ? mp_tpps_ls_kernel<true, 2> : mp_tpps_ls_kernel<false, 2>)
-                           : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>);
+             : a.cost_global
+                 ? (r3 ? (a.colo ? mp_tpps_ls_kernel<true, 3, true> : mp_tpps_ls_kernel<false, 3, true>)
+                       : (a.colo ? mp_tpps_ls_kernel<true, 3> : mp_tpps_ls_kernel<false, 3>))
+             : a.durtab
+                 ? (r3 ? (a.colo ? mp_tpps_ls_kernel<true, 2, true> : mp_tpps_ls_kernel<false, 2, true>)
+                       : (a.colo ? mp_tpps_ls_kernel<true, 2> : mp_tpps_ls_kernel<false, 2>))
+                 : (r3 ? (a.colo ? mp_tpps_ls_kernel<true, 0, true> : mp_tpps_ls_kernel<false, 0, true>)
+                       : (a.colo ? mp_tpps_ls_kernel<true, 0> : mp_tpps_ls_kernel<false, 0>));
     f<<<ctas, threads, smem, s>>>(a, ls);
     ++g_mp_launches;
     return cudaGetLastError();

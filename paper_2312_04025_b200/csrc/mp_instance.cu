@@ -375,6 +375,8 @@ struct mp_instance {
     bool force_offchip = false;  // MP_TUNE_OFFCHIP
     int tpp_kind = 0;           // 1: ready set in registers (tpp_rc entries), 2: in shared memory (capacity tpp_rc)
     int tpp_rc = 0, tpp_threads = 0, tpp_ctas = 0, tpp_smem = 0;
+    int tpp_rb = 4;             // shared-ready-set kernels' row tile: 3-bit words or nibbles (tpp_lane)
+    bool row3_forced = false;   // MP_TUNE_ROW3
     DevBuf tpp_state;
     // streamed host input: a device word {rows ready, wait timeout} written by the copy
     // stream with cuStreamWriteValue32 (driver entry point fetched at run time)
@@ -398,6 +400,11 @@ namespace {
 
 void set_ls_cap(mp_instance *I, int ready_cap_req);
 uint32_t tpp_tab_bytes(const mp_instance *I);
+struct TppLane {
+    int rb, nclk;
+    long long row, bytes;
+};
+TppLane tpp_lane(const mp_instance *I, int cap, int rb);
 
 void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, int ready_cap_req = 0) {
     const int n_ops = I->n_ops, K = I->K;
@@ -517,7 +524,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
     if (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1 && I->cost_mode != 2) {
         const int cap_s = ready_cap_req > 0 ? std::max(1, std::min(I->ready_bound, I->rcap_target))
                                             : std::min(I->ready_bound, std::max(4, I->peak_probe > 0 ? I->peak_probe : 4));
-        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1);
+        const long long lane_s = tpp_lane(I, cap_s, 3).bytes;
         const long long t_s = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.s_rec - 32) / lane_s;
         const long long t_g = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.cost - 32) / lane_s;
         I->cost_global = I->cost_mode == 1 || (2 * std::min<long long>(t_g, MP_TPP_MAX_THREADS) >=
@@ -529,10 +536,18 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         const long long avail_s = static_cast<long long>(MP_TPP_SMEM_MAX) - tpp_tab_bytes(I) - 32;
         const long long base_lane = n_ops + 8LL * (3 * K + 2);
         // shared-memory ready set: 24 B per entry per lane, capacity = the peak (>= 4),
-        // row tile nibble-packed
+        // row tile packed (tpp_lane)
         const int cap_s = ready_cap_req > 0 ? rcap : std::min(I->ready_bound, std::max(4, want));
-        const long long lane_s = (n_ops + 1) / 2 + 8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1);
-        const int Ts = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail_s / lane_s) / 32 * 32));
+        // 3-bit rows (K <= 8) only where they add lanes: their decode costs an instruction
+        // more than a nibble's (C2-K4 already runs 512 lanes with nibbles)
+        auto lanes = [&](const TppLane &l) {
+            return static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail_s / l.bytes) / 32 * 32));
+        };
+        const TppLane l3 = tpp_lane(I, cap_s, 3), l4 = tpp_lane(I, cap_s, 4);
+        I->tpp_rb = (I->row3_forced || lanes(l3) > lanes(l4)) ? l3.rb : 4;
+        const TppLane ln = tpp_lane(I, cap_s, I->tpp_rb);
+        const long long lane_s = ln.bytes;
+        const int Ts = lanes(ln);
         // register ready set: the smallest template >= the peak
         const int rc = want <= 4 ? 4 : (want <= 8 ? 8 : (want <= 16 ? 16 : 0));
         const int Tr = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / base_lane) / 32 * 32));
@@ -544,8 +559,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
             I->tpp_kind = 2;
             I->tpp_rc = cap_s;
             I->tpp_threads = Ts;
-            I->tpp_smem = static_cast<int>(tpp_tab_bytes(I) + ((static_cast<long long>((n_ops + 1) / 2) * Ts + 15) & ~15LL) +
-                                           (8LL * (3 * K + 2) + 24LL * ((cap_s + 1) & ~1)) * Ts);
+            I->tpp_smem = static_cast<int>(tpp_tab_bytes(I) + ((ln.row * Ts + 15) & ~15LL) + (ln.bytes - ln.row) * Ts);
         } else if (rc > 0 && Tr >= 128) {
             I->tpp_kind = 1;
             I->tpp_rc = rc;
@@ -556,6 +570,20 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         I->tpp_ctas = std::min(I->sms, I->main.ctas);
     }
     set_ls_cap(I, ready_cap_req);
+}
+
+// Per-lane shared memory of the shared-ready-set TPP kernels: the row tile (3-bit
+// words for K <= 8 with the round-2 evaluator, else nibbles), the clocks (3K with the
+// round-2 evaluator in colo mode, else 3K + 2) and `cap` (rounded up to even) 24-byte
+// ready entries.  mp_eval.cu tpp_view lays it out from EvalArgs::tpp_rb / tpp_nclk.
+TppLane tpp_lane(const mp_instance *I, int cap, int rb) {
+    TppLane l{};
+    const bool r2 = !I->tpp_round1;
+    l.rb = (r2 && I->K <= 8) ? rb : 4;
+    l.nclk = (r2 && I->colo) ? 3 * I->K : 3 * I->K + 2;
+    l.row = l.rb == 3 ? 8LL * ((I->n_ops + 20) / 21) : (I->n_ops + 1) / 2;
+    l.bytes = l.row + 8LL * l.nclk + 24LL * ((cap + 1) & ~1);
+    return l;
 }
 
 // table bytes the shared-memory-ready-set TPP kernels stage: the duration-table
@@ -569,11 +597,10 @@ uint32_t tpp_tab_bytes(const mp_instance *I) {
 // (local search runs at the group kernel's capacity); threads = 0 if it does not fit
 void tpps_shape(const mp_instance *I, int cap, int *threads, int *smem) {
     const long long avail = static_cast<long long>(MP_TPP_SMEM_MAX) - tpp_tab_bytes(I) - 32;
-    const long long row = (I->n_ops + 1) / 2;  // nibble-packed row tile
-    const long long per_lane = row + 8LL * (3 * I->K + 2) + 24LL * ((cap + 1) & ~1);  // even slot count
-    const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / per_lane) / 32 * 32));
+    const TppLane ln = tpp_lane(I, cap, I->tpp_rb);
+    const int T = static_cast<int>(std::min<long long>(MP_TPP_MAX_THREADS, std::max(0LL, avail / ln.bytes) / 32 * 32));
     *threads = T >= 64 ? T : 0;
-    *smem = static_cast<int>(tpp_tab_bytes(I) + ((row * T + 15) & ~15LL) + (per_lane - row) * T);
+    *smem = static_cast<int>(tpp_tab_bytes(I) + ((ln.row * T + 15) & ~15LL) + (ln.bytes - ln.row) * T);
 }
 
 // Local search rejects a proposal whose ready set exceeds ls_cap in every kernel,
@@ -605,6 +632,14 @@ EvalArgs base_args(const mp_instance *I, bool wide) {
     a.durtab = (I->dur_classes > 0 && !I->durtab_off) ? 1 : 0;
     a.tpp_stage = I->tpp_kind == 2 ? tpp_tab_bytes(I) : I->to.bytes;
     a.cost_global = (a.durtab && I->cost_global && I->tpp_kind == 2) ? 1 : 0;
+    if (I->tpp_kind == 2) {
+        const TppLane ln = tpp_lane(I, 1, I->tpp_rb);
+        a.tpp_rb = ln.rb;
+        a.tpp_nclk = ln.nclk;
+    } else {
+        a.tpp_rb = 8;
+        a.tpp_nclk = 3 * I->K + 2;
+    }
     a.tpp_alt = I->tpp_round1 ? 1 : 0;
     a.rcap = wide ? std::max(1, I->ready_bound) : I->main_rcap;
     a.groups_per_cta = wide ? I->wide.groups_per_cta : I->main.groups_per_cta;
@@ -1032,6 +1067,7 @@ int32_t mp_instance_tune(mp_instance *I, int32_t group_lanes, int32_t lanes_used
     I->force_offchip = (flags & MP_TUNE_OFFCHIP) != 0;
     I->durtab_off = (flags & MP_TUNE_NO_DURTAB) != 0;
     I->cost_mode = (flags & MP_TUNE_COST_GLOBAL) ? 1 : ((flags & MP_TUNE_COST_SMEM) ? 2 : 0);
+    I->row3_forced = (flags & MP_TUNE_ROW3) != 0;
     choose_shapes(I, group_lanes, lanes_used, ctas_per_sm, ready_cap);
     return MP_OK;
 }

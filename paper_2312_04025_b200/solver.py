@@ -144,17 +144,18 @@ class Instance:
     def tune(self, group_lanes: int = 0, ctas_per_sm: int = 0, ready_cap: int = 0, colo: bool = True,
              lanes_used: int = 0, tpp: bool = True, tpp_registers: bool = False,
              offchip: bool = False, tpp_round1: bool = False, durtab: bool = True,
-             costs: str = "auto") -> None:
+             costs: str = "auto", row3: bool = False) -> None:
         """Launch-shape knobs: evaluation results never depend on them.  With
         automatic ``group_lanes``/``lanes_used`` and ``tpp`` the thread-per-placement
         kernel runs when the calibrated ready set fits its register capacity.
         ``ready_cap`` also fixes the local-search capacity (a proposal whose ready
         set exceeds it is rejected), the one knob local-search results depend on.
         ``costs``: where the duration-table kernel reads op costs ("auto": shared
-        memory unless reading them through L1 fits 1.5x the lanes)."""
+        memory unless reading them through L1 fits 1.5x the lanes); ``row3`` forces the
+        3-bit row tile (K <= 8) that is otherwise used only where it fits more lanes."""
         flags = ((0 if colo else 1) | (0 if tpp else 2) | (4 if tpp_registers else 0) | (8 if offchip else 0)
                  | (16 if tpp_round1 else 0) | (0 if durtab else 32)
-                 | {"auto": 0, "global": 64, "smem": 128}[costs])
+                 | {"auto": 0, "global": 64, "smem": 128}[costs] | (256 if row3 else 0))
         if self._lib.mp_instance_tune(self._h, group_lanes, lanes_used, ctas_per_sm, ready_cap, flags) != 0:
             raise ValueError("group_lanes in {0,1,2,4,8,16,32}; lanes_used a multiple of it, <= 32")
 

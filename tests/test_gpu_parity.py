@@ -257,7 +257,8 @@ TPP_SHAPES = [dict(), dict(colo=False), dict(ready_cap=3), dict(ready_cap=6, col
               dict(tpp_registers=True), dict(tpp_registers=True, colo=False), dict(tpp_registers=True, ready_cap=3),
               dict(tpp_registers=True, ready_cap=12), dict(tpp_round1=True), dict(tpp_round1=True, ready_cap=3),
               dict(durtab=False), dict(durtab=False, colo=False, ready_cap=3), dict(costs="global"),
-              dict(costs="global", colo=False, ready_cap=3)]
+              dict(costs="global", colo=False, ready_cap=3), dict(row3=True), dict(row3=True, colo=False),
+              dict(row3=True, costs="global", ready_cap=3), dict(row3=True, durtab=False)]
 
 
 @pytest.mark.parametrize("flavor", ["plain", "tight", "ties", "zero"])
@@ -300,7 +301,7 @@ def test_eval_vs_oracle_workloads(oracle_mod, name):
         want, wst = orc.eval_batch(rows, threads=8)
         for shape in (dict(), dict(group_lanes=1, lanes_used=16), dict(group_lanes=8), dict(group_lanes=32, colo=False),
                       dict(ready_cap=3), dict(tpp=False), dict(tpp_registers=True), dict(tpp_round1=True),
-                      dict(durtab=False), dict(costs="global"), dict(costs="smem")):
+                      dict(durtab=False), dict(costs="global"), dict(costs="smem"), dict(row3=True)):
             inst.tune(**shape)
             ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
             assert np.array_equal(st, wst) and np.array_equal(bits(ms), bits(want)), (name, shape)
@@ -353,7 +354,7 @@ def test_local_search_reverifies_and_is_deterministic(oracle_mod):
         seed_ms = mp.evaluate_batch(inst, seeds)
         a = mp.local_search(inst, seeds, chains=512, moves=48, seed=7)
         for shape in (dict(group_lanes=8, colo=False), dict(tpp_registers=True), dict(costs="global"),
-                      dict(durtab=False)):
+                      dict(durtab=False), dict(row3=True)):
             inst.tune(**shape)
             b = mp.local_search(inst, seeds, chains=512, moves=48, seed=7)
             assert np.array_equal(a[0], b[0]) and a[1] == b[1] and a[2] == b[2], shape
