@@ -483,7 +483,9 @@ def roofline(P, n_ops, n_flows, t_kern, peaks, ncu, info) -> dict:
       (L2 when the tables are off-chip);
     * hbm: B_hbm = α + 8 bytes (row in, makespan out) against MEASURED_PEAKS.json;
     * issue: issued warp-instructions per cycle / 4 schedulers per SM, from the ncu
-      capture of this exact source tree (null when the capture is stale)."""
+      capture of this exact source tree (null when the capture is stale);
+    * alu_pipe / l1_data_pipe: busy fraction of the integer ALU pipe and of the L1 data
+      pipe (shared-memory and global wavefronts) in the same capture."""
     hbm_peak, hbm_src = measured_hbm_peak()
     b_hbm = n_ops + 8
     b_tab = 8 * n_ops + 24 * n_flows
@@ -502,6 +504,11 @@ def roofline(P, n_ops, n_flows, t_kern, peaks, ncu, info) -> dict:
         ib = ncu.get("issue_slots_busy")
         fr["issue"] = {"achieved": ncu.get("ipc_issued"), "peak": 4.0, "unit": "warp-inst/clk/SM", "frac": ib,
                        "inst_per_placement": ncu.get("inst_per_row"), "source": ncu.get("source")}
+        # the two pipes the branch-free dispatch saturates first (ncu pct_of_peak, same capture)
+        for key, name in (("alu_pipe_busy", "alu_pipe"), ("l1_data_pipe_busy", "l1_data_pipe")):
+            if ncu.get(key) is not None:
+                fr[name] = {"achieved": ncu[key], "peak": 1.0, "unit": "fraction of peak cycles",
+                            "frac": ncu[key], "source": ncu.get("source")}
     bound = max(fr, key=lambda k: fr[k]["frac"] or 0.0)
     top = fr[bound]
     traffic = None

@@ -34,6 +34,11 @@ METRICS = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_conflicts",
     "launch__registers_per_thread": "regs",
     "smsp__thread_inst_executed_per_inst_executed.ratio": "threads_per_inst",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pct",
+    "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed": "l1_wavefronts_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefronts_pct",
 }
 
 
@@ -96,6 +101,13 @@ def main():
         "smem_conflict_share": (m["smem_conflicts"] / m["smem_wavefronts"]) if m["smem_wavefronts"] else None,
         "registers": m["regs"],
         "threads_per_inst": m["threads_per_inst"],
+        # pipe utilisation: the integer ALU pipe (selects, logic, compares: half the issue
+        # rate of the FMA pipe) and the L1 data pipe (shared-memory + global wavefronts)
+        "alu_pipe_busy": m["alu_pct"] / 100 if m["alu_pct"] is not None else None,
+        "fma_pipe_busy": m["fma_pct"] / 100 if m["fma_pct"] is not None else None,
+        "fp64_pipe_busy": m["fp64_pct"] / 100 if m["fp64_pct"] is not None else None,
+        "l1_data_pipe_busy": m["l1_wavefronts_pct"] / 100 if m["l1_wavefronts_pct"] is not None else None,
+        "smem_data_pipe_busy": m["smem_wavefronts_pct"] / 100 if m["smem_wavefronts_pct"] is not None else None,
         "source": f"ncu --set full --clock-control none ({Path(a.report).name}), last {a.kernel} launch",
         "source_hash": source_hash(),
         "so_sha256": hashlib.sha256(so.read_bytes()).hexdigest()[:16] if so.exists() else None,
