@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import CycleCreationError, CycleError, UnknownEdgeError
-from .graph import CompGraph, FlowEdge, OpNode, Tag, _bulk_objects, _make_edge, _make_opnode, find_cycle, validate_dag
+from .graph import CompGraph, FlowEdge, OpNode, Tag, _bulk_objects, find_cycle, validate_dag
 from .profiles import CostOverrides
 
 FUSE_JOINER = "∘"  # joins member types in a fused node's op_type (fusion.py:23)
@@ -116,51 +116,84 @@ _A_SEQ, _A_TAG, _A_MEM, _A_CT = (attrgetter("type_seq"), attrgetter("tag"), attr
                                   attrgetter("compute_time"))
 
 
-class _Flat:
-    """Array form of a coarsening problem (mp_coarsen_input)."""
+class _NodeArrays:
+    """Graph-intrinsic part of the flat coarsening input, cached on the (immutable)
+    CompGraph: interned node type sequences (node types get the first ids, in node
+    order — exactly as the per-call interning numbers them), tags, memory and the
+    cost matrix over the devices the nodes name."""
 
-    def __init__(self, g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None):
+    __slots__ = ("types", "seq_beg", "seq", "tag", "mem", "cost", "devices")
+
+    def __init__(self, g: CompGraph):
         nodes = g.nodes
-        dg = g.csr()
         V = len(nodes)
         seqs = list(map(_A_SEQ, nodes))
         flat_types = list(chain.from_iterable(seqs))
-        for r in rules:
-            flat_types.extend(r.pattern)
-        if overrides is not None:
-            for (s, _k) in overrides.entries:
-                flat_types.extend(s)
-        types = {t: k for k, t in enumerate(dict.fromkeys(flat_types))}
+        self.types = {t: k for k, t in enumerate(dict.fromkeys(flat_types))}
         lens = np.fromiter(map(len, seqs), dtype=np.int32, count=V)
-        seq_beg = np.zeros(V + 1, np.int32)
-        np.cumsum(lens, out=seq_beg[1:])
-        total = int(seq_beg[-1])
-        seq = np.fromiter(map(types.__getitem__, flat_types[:total]), dtype=np.int32, count=total)
-        tag = np.fromiter(map(_TAG_CODE.__getitem__, map(_A_TAG, nodes)), dtype=np.int32, count=V)
-        mem = np.fromiter(map(_A_MEM, nodes), dtype=np.int64, count=V)
+        self.seq_beg = np.zeros(V + 1, np.int32)
+        np.cumsum(lens, out=self.seq_beg[1:])
+        total = int(self.seq_beg[-1])
+        self.seq = np.fromiter(map(self.types.__getitem__, flat_types), dtype=np.int32, count=total)
+        self.tag = np.fromiter(map(_TAG_CODE.__getitem__, map(_A_TAG, nodes)), dtype=np.int32, count=V)
+        self.mem = np.fromiter(map(_A_MEM, nodes), dtype=np.int64, count=V)
         cts = list(map(_A_CT, nodes))
-        devs = set()
         keys = list(map(tuple, cts))
         first = keys[0] if keys else ()
         uniform = keys.count(first) == len(keys)
-        if uniform:
-            devs.update(first)
-        else:
-            for ct in cts:
-                devs.update(ct)
-        if overrides is not None:
-            devs.update(k for (_, k) in overrides.entries)
+        devs = set(first) if uniform else set().union(*cts)
         self.devices = sorted(devs)
-        dindex = {d: i for i, d in enumerate(self.devices)}
         D = len(self.devices)
         if uniform and V and list(first) == self.devices:
             cost = np.fromiter(chain.from_iterable(map(dict.values, cts)), dtype=np.float64,
                                count=V * D).reshape(V, max(D, 1))
         else:
+            dindex = {d: i for i, d in enumerate(self.devices)}
             cost = np.full((V, max(D, 1)), np.nan)
             for i, ct in enumerate(cts):
                 for k, t in ct.items():
                     cost[i, dindex[k]] = float(t)
+        self.cost = np.ascontiguousarray(cost)
+
+    @staticmethod
+    def of(g: CompGraph) -> "_NodeArrays":
+        na = getattr(g, "_gcof_node_arrays", None)
+        if na is None:
+            na = _NodeArrays(g)
+            g._gcof_node_arrays = na
+        return na
+
+
+class _Flat:
+    """Array form of a coarsening problem (mp_coarsen_input)."""
+
+    def __init__(self, g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None):
+        na = _NodeArrays.of(g)
+        dg = g.csr()
+        V = len(g)
+        types = dict(na.types)
+        for r in rules:
+            for t in r.pattern:
+                types.setdefault(t, len(types))
+        if overrides is not None:
+            for (sq, _k) in overrides.entries:
+                for t in sq:
+                    types.setdefault(t, len(types))
+        total = int(na.seq_beg[-1])
+        devices = na.devices
+        cost = na.cost
+        if overrides is not None:
+            extra = sorted({k for (_, k) in overrides.entries} - set(devices))
+            if extra:  # override-only devices: NaN columns (no member has a time there)
+                devices = sorted(set(devices) | set(extra))
+                full = np.full((V, len(devices)), np.nan)
+                pos = [devices.index(d) for d in na.devices]
+                if na.devices:
+                    full[:, pos] = na.cost[:, :len(na.devices)]
+                cost = full
+        self.devices = devices
+        dindex = {d: i for i, d in enumerate(self.devices)}
+        D = len(self.devices)
         rb = np.zeros(len(rules) + 1, np.int32)
         rt = []
         rid = np.empty(len(rules), np.int32)
@@ -173,14 +206,14 @@ class _Flat:
         odev = []
         otime = []
         if overrides is not None:
-            for (s, k), t in overrides.entries.items():
-                ot.extend(types[x] for x in s)
+            for (sq, k), t in overrides.entries.items():
+                ot.extend(types[x] for x in sq)
                 ob.append(len(ot))
                 odev.append(dindex[k])
                 otime.append(float(t))
         self.keep = [
-            dg.ids, seq_beg, seq if total else np.zeros(1, np.int32), tag, mem, np.ascontiguousarray(cost),
-            dg.esrc, dg.edst, dg.payload, rid, rb, np.asarray(rt or [0], np.int32),
+            dg.ids, na.seq_beg, na.seq if total else np.zeros(1, np.int32), na.tag, na.mem,
+            np.ascontiguousarray(cost), dg.esrc, dg.edst, dg.payload, rid, rb, np.asarray(rt or [0], np.int32),
             np.asarray(ob, np.int32), np.asarray(ot or [0], np.int32), np.asarray(odev or [0], np.int32),
             np.asarray(otime or [0.0], np.float64),
         ]
@@ -219,22 +252,24 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
     N.check(code, err, "mp_coarsen")
     LAST_GCOF["ordered_replay"] = bool(out.ordered_replay)
     try:
+        # views of the native buffers (freed below, after the result no longer needs them;
+        # everything kept is converted to lists / owned arrays while building it)
         nodes_in = g.nodes
         ng, ne = out.n_groups, out.n_edges
         D = len(flat.devices)
-        grp_tag = np.ctypeslib.as_array(out.grp_tag, (ng,)).copy() if ng else np.zeros(0, np.int32)
-        mbeg = np.ctypeslib.as_array(out.mem_beg, (ng + 1,)).copy()
-        members = np.ctypeslib.as_array(out.members, (int(mbeg[-1]),)).copy() if mbeg[-1] else np.zeros(0, np.int32)
-        gmem = np.ctypeslib.as_array(out.grp_mem, (ng,)).copy() if ng else np.zeros(0, np.int64)
-        gcost = (np.ctypeslib.as_array(out.grp_cost, (ng * max(D, 1),)).reshape(ng, max(D, 1)).copy()
-                 if ng else np.zeros((0, 1)))
-        esrc = np.ctypeslib.as_array(out.out_src, (ne,)).copy() if ne else np.zeros(0, np.int32)
-        edst = np.ctypeslib.as_array(out.out_dst, (ne,)).copy() if ne else np.zeros(0, np.int32)
-        epay = np.ctypeslib.as_array(out.out_payload, (ne,)).copy() if ne else np.zeros(0, np.int64)
+        view = np.ctypeslib.as_array
+        grp_tag = view(out.grp_tag, (ng,)) if ng else np.zeros(0, np.int32)
+        mbeg = view(out.mem_beg, (ng + 1,))
+        members = view(out.members, (int(mbeg[-1]),)) if mbeg[-1] else np.zeros(0, np.int32)
+        gmem = view(out.grp_mem, (ng,)) if ng else np.zeros(0, np.int64)
+        gcost = view(out.grp_cost, (ng * max(D, 1),)).reshape(ng, max(D, 1)) if ng else np.zeros((0, 1))
+        esrc = view(out.out_src, (ne,)).copy() if ne else np.zeros(0, np.int32)
+        edst = view(out.out_dst, (ne,)).copy() if ne else np.zeros(0, np.int32)
+        epay = view(out.out_payload, (ne,)).copy() if ne else np.zeros(0, np.int64)
+        with _bulk_objects():
+            return _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay)
     finally:
         lib.mp_coarsen_free(C.byref(out))
-    with _bulk_objects():
-        return _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay)
 
 
 def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay) -> CompGraph:
@@ -249,6 +284,10 @@ def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, 
     mem_l = gmem.tolist()
     tag_l = grp_tag.tolist()
     join = FUSE_JOINER.join
+    tags = [_CODE_TAG[c] for c in range(3)]
+    op_types: dict = {}  # fused type sequences repeat (one per layer kind): join once
+    new = object.__new__
+    setattr_ = object.__setattr__  # OpNode is frozen: install its __dict__ in one call
     for z in range(ng):
         b, e = mb[z], mb[z + 1]
         if e - b == 1:
@@ -269,7 +308,13 @@ def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, 
         row = cost_rows[z]
         cost = ({devices[k]: row[k] for k in range(D) if row[k] == row[k]} if partial[z]
                 else dict(zip(devices, row)))
-        new_nodes.append(_make_opnode(gid, join(seq), mem_l[z], cost, mids, seq, _CODE_TAG[tag_l[z]]))
+        ot = op_types.get(seq)
+        if ot is None:
+            ot = op_types[seq] = join(seq)
+        n = new(OpNode)
+        setattr_(n, "__dict__", {"id": gid, "op_type": ot, "mem_bytes": mem_l[z], "compute_time": cost,
+                                 "members": mids, "type_seq": seq, "tag": tags[tag_l[z]]})
+        new_nodes.append(n)
     # output nodes come in ascending id order, so group indices are node indices
     return CompGraph._from_arrays(new_nodes, esrc, edst, epay)
 
