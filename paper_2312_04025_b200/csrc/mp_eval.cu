@@ -776,10 +776,14 @@ struct TppView {
 // nib: the row tile holds two device indices per byte (shared-memory ready-set
 // variant, K <= 16), (n_ops + 1) / 2 bytes per lane
 // Row tile per lane by a.tpp_rb: 8 = one byte per op, 4 = two ops per byte (low nibble =
-// even op), 3 = 21 ops per 64-bit word (K <= 8); see tpp_row_bytes.
+// even op), 3 = ten 3-bit indices per 32-bit word (K <= 8; one 32-bit shift to decode);
+// mp_instance.cu tpp_lane sizes the same layout.
 __host__ __device__ __forceinline__ size_t tpp_row_bytes_dev(int rb, int n_ops) {
-    return rb == 3 ? 8ULL * ((n_ops + 20) / 21) : (rb == 4 ? static_cast<size_t>((n_ops + 1) / 2) : static_cast<size_t>(n_ops));
+    return rb == 3 ? 4ULL * ((n_ops + 9) / 10) : (rb == 4 ? static_cast<size_t>((n_ops + 1) / 2) : static_cast<size_t>(n_ops));
 }
+
+// x / 10 for 0 <= x < 2^20 as one IMAD.HI (ceil(2^32 / 10); the error x * 0.4 / 2^32 < 0.1)
+__device__ __forceinline__ int div10(int x) { return static_cast<int>(__umulhi(static_cast<unsigned>(x), 429496730u)); }
 
 __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm, bool nib = false) {
     TppView v;
@@ -830,14 +834,14 @@ __device__ __forceinline__ TppView tpp_view(const EvalArgs &a, unsigned char *sm
 // Load one placement row (global byte offset `start`) into this lane's column of
 // the row tile with 16-byte L2 loads; returns true if it names a device >= K.
 // NIB: pack two device indices per byte (low nibble = even op).
-// R3: 21 three-bit device indices per 64-bit word, words lane-interleaved [w][T].
+// R3: ten three-bit device indices per 32-bit word, words lane-interleaved [w][T].
 template <bool NIB = false, bool R3 = false>
 __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *rows, long long rows_bytes,
                                              long long start, bool live) {
     bool bad = false;
     const int n_ops = v.n_ops, T = v.T, tid = v.tid;
-    unsigned long long *row64 = reinterpret_cast<unsigned long long *>(v.rowt) + tid;
-    unsigned long long acc = 0;
+    uint32_t *row32 = reinterpret_cast<uint32_t *>(v.rowt) + tid;
+    uint32_t acc = 0;
     const long long a0 = start & ~15LL;
     const long long a1 = (start + n_ops + 15) & ~15LL;
     const int chunks = live ? static_cast<int>((a1 - a0) >> 4) : 0;
@@ -861,10 +865,10 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
                 bad |= d >= v.K;
                 if constexpr (R3) {
                     const int p = static_cast<int>(pos);
-                    const int w = p / 21, r = p - 21 * w;
-                    acc |= static_cast<unsigned long long>(d & 7u) << (3 * r);
-                    if (r == 20 || p == n_ops - 1) {
-                        row64[w * T] = acc;
+                    const int w = div10(p), r = p - 10 * w;
+                    acc |= static_cast<uint32_t>(d & 7u) << (3 * r);
+                    if (r == 9 || p == n_ops - 1) {
+                        row32[w * T] = acc;
                         acc = 0;
                     }
                 } else if constexpr (NIB) {
@@ -879,7 +883,7 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
     }
     if (!live || bad) {  // keep the lockstep passes in bounds
         if constexpr (R3) {
-            for (int i = 0; i < (n_ops + 20) / 21; ++i) row64[i * T] = 0ULL;
+            for (int i = 0; i < (n_ops + 9) / 10; ++i) row32[i * T] = 0u;
         } else {
             const int nb = NIB ? (n_ops + 1) / 2 : n_ops;
             for (int i = 0; i < nb; ++i) v.rowt[i * T + tid] = 0;
@@ -892,9 +896,8 @@ __device__ __forceinline__ bool tpp_load_row(const TppView &v, const uint8_t *ro
 template <bool R3>
 __device__ __forceinline__ int tpp_row_get(const TppView &v, int i) {
     if constexpr (R3) {
-        const int w = i / 21;
-        return static_cast<int>((reinterpret_cast<const unsigned long long *>(v.rowt)[w * v.T + v.tid] >>
-                                 (3 * (i - 21 * w))) & 7ULL);
+        const int w = div10(i);
+        return static_cast<int>((reinterpret_cast<const uint32_t *>(v.rowt)[w * v.T + v.tid] >> (3 * (i - 10 * w))) & 7u);
     } else {
         return (v.rowt[(i >> 1) * v.T + v.tid] >> ((i & 1) << 2)) & 15;
     }
@@ -903,9 +906,9 @@ __device__ __forceinline__ int tpp_row_get(const TppView &v, int i) {
 template <bool R3>
 __device__ __forceinline__ void tpp_row_set(const TppView &v, int i, int d) {
     if constexpr (R3) {
-        const int w = i / 21, sh = 3 * (i - 21 * w);
-        unsigned long long *c = reinterpret_cast<unsigned long long *>(v.rowt) + w * v.T + v.tid;
-        *c = (*c & ~(7ULL << sh)) | (static_cast<unsigned long long>(d) << sh);
+        const int w = div10(i), sh = 3 * (i - 10 * w);
+        uint32_t *c = reinterpret_cast<uint32_t *>(v.rowt) + w * v.T + v.tid;
+        *c = (*c & ~(7u << sh)) | (static_cast<uint32_t>(d) << sh);
     } else {
         unsigned char *cell = &v.rowt[(i >> 1) * v.T + v.tid];
         const int sh = (i & 1) << 2;
@@ -1489,7 +1492,6 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     const double *__restrict__ T_cost = GC ? reinterpret_cast<const double *>(a.blob + a.to.cost) : v.T_cost;
     auto cost = [&](int x) -> double { return GC ? __ldg(T_cost + x) : T_cost[x]; };
     const unsigned long long *__restrict__ T_rec8 = v.T_rec8;  // TAB: {dst | base << 20, node id}
-    const long long *__restrict__ T_mem = v.T_mem;
     const long long *__restrict__ T_cap = v.T_cap;
     const double *__restrict__ T_bw = v.T_bw;
     const double *__restrict__ T_rbw = v.T_rbw;
@@ -1509,11 +1511,11 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     const int capA = (a.rcap + 1) & ~1;
     unsigned long long *__restrict__ rE = v.rE + v.tid;  // slot s: rE[s * T]; rank / meta at fixed offsets
     const size_t DR = static_cast<size_t>(v.rR - v.rE), DM = static_cast<size_t>(v.rM - v.rE);
-    const unsigned long long *__restrict__ rowl64 = reinterpret_cast<const unsigned long long *>(v.rowt) + v.tid;
+    const uint32_t *__restrict__ rowl32 = reinterpret_cast<const uint32_t *>(v.rowt) + v.tid;
     auto dev = [&](int x) -> int {
         if constexpr (R3) {
-            const int w = static_cast<int>(__umulhi(static_cast<unsigned>(x), 204522253u));  // x / 21
-            return static_cast<int>((rowl64[w * T] >> (3 * (x - 21 * w))) & 7ULL);
+            const int w = div10(x);
+            return static_cast<int>((rowl32[w * T] >> (3 * (x - 10 * w))) & 7u);
         } else {
             return (rowl[(x >> 1) * T] >> ((x & 1) << 2)) & 15;
         }
@@ -1527,7 +1529,20 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     long long over_by = 0;
     for (int k = 0; k < K; ++k) ld[k * T] = 0ULL;
     if (live && !bad) {
-        for (int i = 0; i < n_ops; ++i) ld[dev(i) * T] += static_cast<unsigned long long>(T_mem[i]);
+        // op memory read through L1 (the section is not staged: only this pass reads it)
+        if constexpr (R3) {  // ten indices per word, constant shifts
+            const long long *gmem = reinterpret_cast<const long long *>(a.blob + a.to.mem);
+            for (int w = 0, i0 = 0; i0 < n_ops; ++w, i0 += 10) {
+                const uint32_t word = rowl32[w * T];
+#pragma unroll
+                for (int r = 0; r < 10; ++r)
+                    if (i0 + r < n_ops)
+                        ld[((word >> (3 * r)) & 7u) * T] += static_cast<unsigned long long>(__ldg(gmem + i0 + r));
+            }
+        } else {
+            const long long *gmem = reinterpret_cast<const long long *>(a.blob + a.to.mem);
+            for (int i = 0; i < n_ops; ++i) ld[dev(i) * T] += static_cast<unsigned long long>(__ldg(gmem + i));
+        }
         for (int k = 0; k < K; ++k) {
             const long long l = static_cast<long long>(ld[k * T]);
             if (l > T_cap[k]) {

@@ -298,8 +298,8 @@ TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls, int n_multi, int n_
         return at;
     };
     // staged prefixes of the duration-table TPP kernels: [0, cost) with costs read through
-    // L1 (wide graphs), [0, s_rec) with costs in shared memory; the rest serves the other kernels
-    t.mem = take(8ULL * n_ops);
+    // L1 (wide graphs), [0, mem) with costs in shared memory (they read mem through L1);
+    // the rest serves the other kernels
     t.cap = take(8ULL * K);
     t.out_beg = take(4ULL * (n_ops + 1));
     t.fdst = take(4ULL * n_flows);
@@ -312,6 +312,7 @@ TabOff make_taboff(int n_ops, int n_flows, int K, int n_cls, int n_multi, int n_
     t.fcb = take(n_cls > 0 ? 4ULL * n_flows : 0);
     t.s_rec8 = take(n_cls > 0 ? 8ULL * n_flows : 0);
     t.cost = take(8ULL * n_ops * K);
+    t.mem = take(8ULL * n_ops);
     t.s_rec = take(16ULL * n_flows);
     t.bw = take(8ULL * K * K);
     t.rbw = take(8ULL * K * K);
@@ -525,7 +526,7 @@ void choose_shapes(mp_instance *I, int G_req, int U_req, int ctas_per_sm_req, in
         const int cap_s = ready_cap_req > 0 ? std::max(1, std::min(I->ready_bound, I->rcap_target))
                                             : std::min(I->ready_bound, std::max(4, I->peak_probe > 0 ? I->peak_probe : 4));
         const long long lane_s = tpp_lane(I, cap_s, 3).bytes;
-        const long long t_s = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.s_rec - 32) / lane_s;
+        const long long t_s = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.mem - 32) / lane_s;
         const long long t_g = std::max(0LL, static_cast<long long>(MP_TPP_SMEM_MAX) - I->to.cost - 32) / lane_s;
         I->cost_global = I->cost_mode == 1 || (2 * std::min<long long>(t_g, MP_TPP_MAX_THREADS) >=
                                                3 * std::min<long long>(t_s, MP_TPP_MAX_THREADS));
@@ -581,7 +582,7 @@ TppLane tpp_lane(const mp_instance *I, int cap, int rb) {
     const bool r2 = !I->tpp_round1;
     l.rb = (r2 && I->K <= 8) ? rb : 4;
     l.nclk = (r2 && I->colo) ? 3 * I->K : 3 * I->K + 2;
-    l.row = l.rb == 3 ? 8LL * ((I->n_ops + 20) / 21) : (I->n_ops + 1) / 2;
+    l.row = l.rb == 3 ? 4LL * ((I->n_ops + 9) / 10) : (I->n_ops + 1) / 2;
     l.bytes = l.row + 8LL * l.nclk + 24LL * ((cap + 1) & ~1);
     return l;
 }
@@ -589,7 +590,7 @@ TppLane tpp_lane(const mp_instance *I, int cap, int rb) {
 // table bytes the shared-memory-ready-set TPP kernels stage: the duration-table
 // variant never reads fpay (the last section)
 uint32_t tpp_tab_bytes(const mp_instance *I) {
-    if (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1) return I->cost_global ? I->to.cost : I->to.s_rec;
+    if (I->dur_classes > 0 && !I->durtab_off && !I->tpp_round1) return I->cost_global ? I->to.cost : I->to.mem;
     return I->to.bytes;
 }
 
