@@ -1789,9 +1789,11 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                     *gm(k_[u]) = make_double2(ej, bitsd(static_cast<unsigned long long>(tie_new) |
                                                         (static_cast<unsigned long long>(np) << 32)));
                 const bool op_ins = op_upd & (!multi | (np == 0u));
-                // fdur is +0.0 unless a flow enters (an op update is co-located or comes from a
-                // flow), and +0.0 + rj == rj bit for bit (rj >= +0.0): no select for the rank
-                insert(flow_ins | op_ins, dbits(flow_ins ? end : ej), dbits(fdur + rj),
+                // no selects for est and rank: a flow that enters loaded no multi-input state
+                // (cur = +0.0), so ej == end for it (end >= +0.0); fdur is +0.0 unless a flow
+                // enters (an op update is co-located or comes from a flow), and +0.0 + rj == rj
+                // bit for bit (rj >= +0.0)
+                insert(flow_ins | op_ins, dbits(ej), dbits(fdur + rj),
                        flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (op_r2(dj) << 26)),
                        flow_ins ? pid : (multi ? tie_new : tj));
             }
