@@ -1729,7 +1729,7 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         // becomes NaN (never taken)
         const int last = nr - 1;
         if (!done) {
-            if (bs != last) {
+            {  // bs == last copies the entry onto itself
                 unsigned long long *h = rE + bs * T;
                 const unsigned long long *l = rE + last * T;
                 h[0] = l[0];
@@ -1774,9 +1774,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                     fdur = (isop & cross) ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
                 }
                 const double rj = rj_[u];
-                const uint32_t fmeta = pid | (cross ? ((static_cast<uint32_t>(K + d) << 20) |
-                                                       (static_cast<uint32_t>(2 * K + dj) << 26))
-                                                    : ((RZ << 20) | (RZ << 26)));
+                // (colo: a flow enters only when it crosses devices, so no select)
+                const uint32_t chan = (static_cast<uint32_t>(K + d) << 20) | (static_cast<uint32_t>(2 * K + dj) << 26);
+                const uint32_t fmeta = pid | ((COLO | cross) ? chan : ((RZ << 20) | (RZ << 26)));
                 // multi-input ops keep npred / est / gate id
                 const double cur = cur_[u];
                 const uint32_t ct = static_cast<uint32_t>(tn_[u]);
