@@ -1783,7 +1783,8 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 const uint32_t np = static_cast<uint32_t>(tn_[u] >> 32) - 1u;
                 const uint32_t tj = via_colo ? pid : static_cast<uint32_t>(j);
                 const bool up = end > cur;
-                const double ej = multi ? (up ? end : cur) : end;
+                // a consumer without multi-input state has cur = +0.0 <= end: max(end, cur) == end
+                const double ej = up ? end : cur;
                 const uint32_t tie_new = up ? tj : ((via_colo & (end == cur) & (pid > ct)) ? pid : ct);
                 if (op_upd & multi)
                     *gm(k_[u]) = make_double2(ej, bitsd(static_cast<unsigned long long>(tie_new) |
@@ -1795,7 +1796,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 // bit for bit (rj >= +0.0)
                 insert(flow_ins | op_ins, dbits(ej), dbits(fdur + rj),
                        flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (op_r2(dj) << 26)),
-                       flow_ins ? pid : (multi ? tie_new : tj));
+                       // colo mode: every end > 0 (all durations > 0), so up holds for a
+                       // consumer without multi-input state and tie_new == tj
+                       flow_ins ? pid : ((COLO | multi) ? tie_new : tj));
             }
         }
         done = done | ovf | (nr == 0);
