@@ -1766,9 +1766,11 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 const bool flow_ins = act & isop & !via_colo;  // a flow enters the ready set
                 const bool op_upd = act & !flow_ins;           // j's npred / est / gate change
                 double fdur;
-                if constexpr (TAB) {  // the table's diagonal is 0.0
-                    const double du = T_fdur[cb_[u] + d * K + dj];
-                    fdur = isop ? du : 0.0;
+                if constexpr (TAB) {
+                    // predicated: only lanes whose item is a crossing flow touch the table (idle
+                    // lanes' clamped indices caused most of its bank conflicts)
+                    fdur = 0.0;
+                    if (act & isop & cross) fdur = T_fdur[cb_[u] + d * K + dj];
                 } else {
                     const int bi2 = cross ? d * K + dj : 0;     // computed unconditionally, selected
                     fdur = (isop & cross) ? div_bw(pay_[u], T_bw[bi2], T_rbw[bi2], fast) : 0.0;
