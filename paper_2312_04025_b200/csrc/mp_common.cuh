@@ -122,6 +122,11 @@ struct EvalArgs {
 // Wait (lane 0 of a warp) until rows [.., need) of a streamed batch have landed.
 __device__ __forceinline__ void wait_rows(const EvalArgs &a, unsigned long long need) {
     if (!a.rows_ready) return;
+    {  // common case: the batch has landed; the global timer is read only when waiting
+        unsigned int v;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rows_ready) : "memory");
+        if (v >= need) return;
+    }
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {

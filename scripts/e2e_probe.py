@@ -1,5 +1,7 @@
 """Where the e2e time goes: H2D bandwidth from pinned memory, and wall time of
-the host-pointer (streamed) vs device-pointer argmin calls on C2."""
+the host-pointer (streamed) vs device-pointer argmin calls on C2-K8, plus the
+device-pointer call with a concurrent 278 MB H2D copy on another stream (the
+copy's interference alone) and with the 8 MB makespan read-back."""
 import ctypes as C
 import sys
 import time
@@ -13,7 +15,7 @@ import paper_2312_04025_b200 as mp  # noqa: E402
 from paper_2312_04025_b200 import _native as N  # noqa: E402
 from paper_2312_04025_b200 import workloads  # noqa: E402
 
-w = workloads.c2(4)
+w = workloads.c2(8)
 coarse = mp.gcof(w.raw, w.rules)
 inst = mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster))
 P = 1 << 20
@@ -46,13 +48,55 @@ def call(host):
     N.check(code, err)
 
 
-for host in (False, True, False, True):
+side = torch.cuda.Stream()
+d2 = torch.empty_like(h, device="cuda")
+
+
+def timed(label, fn, n=5):
     for _ in range(2):
-        call(host)
+        fn()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(5):
-        call(host)
+    for _ in range(n):
+        fn()
     torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / 5
-    print(f"{'host (streamed)' if host else 'device ptrs'}: {dt * 1e3:.2f} ms/call, {P / dt / 1e6:.1f} M placements/s")
+    dt = (time.perf_counter() - t0) / n
+    print(f"{label}: {dt * 1e3:.2f} ms/call, {P / dt / 1e6:.1f} M placements/s", flush=True)
+
+
+def dev_with_copy():
+    with torch.cuda.stream(side):
+        d2.copy_(h, non_blocking=True)
+    call(False)
+    side.synchronize()
+
+
+def dev_with_readback():
+    call(False)
+    hm.copy_(dm, non_blocking=True)
+
+
+def gpu_span(label, fn, n=5):
+    """GPU-side span of the call (events on its stream) next to its wall time."""
+    fn()
+    torch.cuda.synchronize()
+    spans, walls = [], []
+    for _ in range(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(s)
+        fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        walls.append((time.perf_counter() - t0) * 1e3)
+        spans.append(e0.elapsed_time(e1))
+    print(f"{label}: GPU span {min(spans):.2f} ms, wall {min(walls):.2f} ms", flush=True)
+
+
+gpu_span("device ptrs", lambda: call(False))
+gpu_span("host (streamed)", lambda: call(True))
+for _ in range(2):
+    timed("device ptrs", lambda: call(False))
+    timed("device ptrs + 8 MB makespan read-back", dev_with_readback)
+    timed("device ptrs + concurrent 278 MB H2D copy", dev_with_copy)
+    timed("host (streamed)", lambda: call(True))
