@@ -1587,14 +1587,17 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
     for (int k = 0; k < a.tpp_nclk; ++k) clk[k * T] = 0.0;
     const unsigned long long NAN_BITS = 0xfff8000000000000ULL;
     const uint32_t SZ = COLO ? 0u : RZ;  // vacated slots read any clock (their NaN est is never taken)
-    const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (SZ << 20) | (SZ << 26));
+    // entry meta word: low half = node | r1 << 26, high half = tie | r2 << 26 (r1 / r2: the clock
+    // slots the key reads); both slots come out with one IMAD.HI each (FMA pipe, not ALU)
+    const unsigned long long SENT_M = static_cast<unsigned long long>(MP_NODE_MASK | (SZ << 26)) |
+                                      (static_cast<unsigned long long>(SZ << 26) << 32);
     for (int s = 0; s < capA; ++s) {
         rE[s * T] = NAN_BITS;
         rE[DM + s * T] = SENT_M;
     }
     int nr = 0;
     bool ovf = false;
-    auto insert = [&](bool ins, unsigned long long est, unsigned long long rk, uint32_t meta, uint32_t tie) {
+    auto insert = [&](bool ins, unsigned long long est, unsigned long long rk, uint32_t lo, uint32_t hi) {
         // bitwise logic throughout the dispatch loop: short-circuit forms compile
         // to branches (BSSY/BSYNC) that measured 6-15 % slower
         const bool room = nr < cap;
@@ -1603,16 +1606,16 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
             unsigned long long *p = rE + nr * T;
             p[0] = est;
             p[DR] = rk;
-            p[DM] = static_cast<unsigned long long>(meta) | (static_cast<unsigned long long>(tie) << 32);
+            p[DM] = static_cast<unsigned long long>(lo) | (static_cast<unsigned long long>(hi) << 32);
         }
         nr += (ins & room) ? 1 : 0;
     };
     if (alive) {
         for (int t = 0; t < a.n_src; ++t) {
             const int i = static_cast<int>(T_srcs[t]);
-            insert(true, 0ULL, dbits(GC ? __ldcg(grank(i)) : *grank(i)),
-                   static_cast<uint32_t>(i) | (static_cast<uint32_t>(dev(i)) << 20) | (op_r2(dev(i)) << 26),
-                   static_cast<uint32_t>(i));
+            const uint32_t di = static_cast<uint32_t>(dev(i));
+            insert(true, 0ULL, dbits(GC ? __ldcg(grank(i)) : *grank(i)), static_cast<uint32_t>(i) | (di << 26),
+                   static_cast<uint32_t>(i) | (op_r2(di) << 26));
         }
     }
     bool done = !alive || ovf;
@@ -1630,12 +1633,12 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
             const double es = bitsd(q[0]);
             const double rs = bitsd(q[DR]);
             const unsigned long long mt = q[DM];
-            const uint32_t m = static_cast<uint32_t>(mt);
-            const double c1 = clk[((m >> 20) & 63u) * T];
-            const double c2 = clk[(m >> 26) * T];
+            const uint32_t m = static_cast<uint32_t>(mt), h = static_cast<uint32_t>(mt >> 32);
+            const double c1 = clk[__umulhi(m, 64u) * T];  // m >> 26
+            const double c2 = clk[__umulhi(h, 64u) * T];
             double e = c1 > es ? c1 : es;  // NaN es stays NaN: never taken
             e = c2 > e ? c2 : e;
-            const uint32_t id = (COLO & (e == es)) ? static_cast<uint32_t>(mt >> 32) : (m & MP_NODE_MASK);
+            const uint32_t id = ((COLO & (e == es)) ? h : m) & MP_NODE_MASK;
             const bool take = (e < be) | ((e == be) & ((rs > br) | ((rs == br) & (id < bi))));
             be = take ? e : be;
             br = take ? rs : br;
@@ -1653,9 +1656,10 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 for (int u = 0; u < 2; ++u) scan_slot(p + u * T, s + u);
             }
         }
-        const uint32_t bm = static_cast<uint32_t>(rE[DM + bs * T]);
+        const unsigned long long bmh = rE[DM + bs * T];
+        const uint32_t bm = static_cast<uint32_t>(bmh), bh = static_cast<uint32_t>(bmh >> 32);
         const int node = static_cast<int>(bm & MP_NODE_MASK);
-        const uint32_t r1 = (bm >> 20) & 63u, r2 = bm >> 26;
+        const uint32_t r1 = __umulhi(bm, 64u), r2 = __umulhi(bh, 64u);
         // a finished lane may have read a vacated slot (any node id): treat it as an
         // op with no successors so every table index below stays in range
         const bool isop = done | (node < n_ops);
@@ -1777,8 +1781,9 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 }
                 const double rj = rj_[u];
                 // (colo: a flow enters only when it crosses devices, so no select)
-                const uint32_t chan = (static_cast<uint32_t>(K + d) << 20) | (static_cast<uint32_t>(2 * K + dj) << 26);
-                const uint32_t fmeta = pid | ((COLO | cross) ? chan : ((RZ << 20) | (RZ << 26)));
+                const bool chan = COLO | cross;  // colo: a flow enters only when it crosses devices
+                const uint32_t flo = pid | ((chan ? static_cast<uint32_t>(K + d) : RZ) << 26);
+                const uint32_t fhi = pid | ((chan ? static_cast<uint32_t>(2 * K + dj) : RZ) << 26);
                 // multi-input ops keep npred / est / gate id
                 const double cur = cur_[u];
                 const uint32_t ct = static_cast<uint32_t>(tn_[u]);
@@ -1797,10 +1802,10 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                 // enters (an op update is co-located or comes from a flow), and +0.0 + rj == rj
                 // bit for bit (rj >= +0.0)
                 insert(flow_ins | op_ins, dbits(ej), dbits(fdur + rj),
-                       flow_ins ? fmeta : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (op_r2(dj) << 26)),
+                       flow_ins ? flo : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 26)),
                        // colo mode: every end > 0 (all durations > 0), so up holds for a
                        // consumer without multi-input state and tie_new == tj
-                       flow_ins ? pid : ((COLO | multi) ? tie_new : tj));
+                       (flow_ins ? fhi : (((COLO | multi) ? tie_new : tj) | (op_r2(static_cast<uint32_t>(dj)) << 26))));
             }
         }
         done = done | ovf | (nr == 0);
