@@ -254,7 +254,6 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
     try:
         # views of the native buffers (freed below, after the result no longer needs them;
         # everything kept is converted to lists / owned arrays while building it)
-        nodes_in = g.nodes
         ng, ne = out.n_groups, out.n_edges
         D = len(flat.devices)
         view = np.ctypeslib.as_array
@@ -266,19 +265,44 @@ def gcof(g: CompGraph, rules: FusionRuleSet, overrides: CostOverrides | None = N
         esrc = view(out.out_src, (ne,)).copy() if ne else np.zeros(0, np.int32)
         edst = view(out.out_dst, (ne,)).copy() if ne else np.zeros(0, np.int32)
         epay = view(out.out_payload, (ne,)).copy() if ne else np.zeros(0, np.int64)
-        with _bulk_objects():
-            return _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay)
+        return _gcof_result(g, flat, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay)
     finally:
         lib.mp_coarsen_free(C.byref(out))
 
 
-def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay) -> CompGraph:
+def _gcof_result(g, flat, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst, epay) -> CompGraph:
     """The coarsened CompGraph from the native output arrays (node by node as the
-    reference builds it; unfused nodes are the input objects themselves)."""
-    new_nodes = []
+    reference builds it; unfused nodes are the input objects themselves).  The node
+    ids and the edge arrays are ready at once; the OpNode objects are built on first
+    use (the next stage — an Instance — reads the cost / memory arrays attached as
+    ``_gcof_cost_arrays`` instead).  ``mbeg``..``grp_tag`` may be views of native
+    buffers: everything kept is copied here."""
+    ids_in = np.asarray(g.csr().ids)
+    if ng:
+        mb = np.array(mbeg[: ng + 1], dtype=np.int64)
+        mem_idx = np.array(members[: int(mb[-1])], dtype=np.int64)
+        ids = ids_in[np.minimum.reduceat(mem_idx, mb[:-1])].tolist()  # id = the smallest member id
+    else:
+        mb, mem_idx, ids = np.zeros(1, np.int64), np.zeros(0, np.int64), []
+    cost = np.array(gcost, dtype=np.float64).reshape(ng, max(D, 1))
+    gmem_c = np.array(gmem, dtype=np.int64)
+    tag_c = np.array(grp_tag, dtype=np.int32)
+    devices = flat.devices
+
+    def build() -> dict:
+        with _bulk_objects():
+            return _gcof_nodes(g.nodes, ng, D, devices, mb, mem_idx, gmem_c, cost, tag_c)
+
+    out = CompGraph._from_lazy(ids, build, esrc, edst, epay)
+    out._gcof_cost_arrays = (devices, cost, gmem_c)
+    return out
+
+
+def _gcof_nodes(nodes_in, ng, D, devices, mbeg, members, gmem, gcost, grp_tag) -> dict:
+    """{id: OpNode} of the coarsened graph (fusion.py:221-240 node by node)."""
+    new_nodes = {}
     mb = mbeg.tolist()
     mlist = members.tolist()
-    devices = flat.devices
     cost_rows = gcost.tolist()
     partial = np.isnan(gcost).any(axis=1).tolist() if ng else []  # a device some member lacks
     mem_l = gmem.tolist()
@@ -291,7 +315,8 @@ def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, 
     for z in range(ng):
         b, e = mb[z], mb[z + 1]
         if e - b == 1:
-            new_nodes.append(nodes_in[mlist[b]])
+            n = nodes_in[mlist[b]]
+            new_nodes[n.id] = n
             continue
         if e - b == 2:
             p0, p1 = nodes_in[mlist[b]], nodes_in[mlist[b + 1]]
@@ -314,9 +339,8 @@ def _gcof_result(g, flat, nodes_in, ng, D, mbeg, members, gmem, gcost, grp_tag, 
         n = new(OpNode)
         setattr_(n, "__dict__", {"id": gid, "op_type": ot, "mem_bytes": mem_l[z], "compute_time": cost,
                                  "members": mids, "type_seq": seq, "tag": tags[tag_l[z]]})
-        new_nodes.append(n)
-    # output nodes come in ascending id order, so group indices are node indices
-    return CompGraph._from_arrays(new_nodes, esrc, edst, epay)
+        new_nodes[gid] = n
+    return new_nodes
 
 
 def _combined_cost(parts, seq, overrides):

@@ -74,21 +74,33 @@ class Instance:
         self.op_ids = [int(x) for x in dg.ids]
         K = len(self.device_ids)
         n = len(self.op_ids)
-        cost = np.empty((n, K), dtype=np.float64)
-        for i, nid in enumerate(self.op_ids):
-            ct = gc.node(nid).compute_time
-            for k, dev in enumerate(self.device_ids):
-                t = ct.get(dev)
-                if t is None:
-                    if _fill_missing is None:
-                        raise MissingCostError(nid, dev)
-                    t = _fill_missing
-                cost[i, k] = t
-        if np.isnan(cost).any():
-            i, k = map(int, np.argwhere(np.isnan(cost))[0])
-            raise ValueError(f"op {self.op_ids[i]} has a NaN compute time on device {self.device_ids[k]}; "
-                             "NaN costs are not supported")
-        mem = np.asarray([gc.node(i).mem_bytes for i in self.op_ids], dtype=np.int64)
+        fast = getattr(gc, "_gcof_cost_arrays", None)  # a GCOF output: its cost / memory arrays
+        if fast is not None:
+            devs, gcost, gmem = fast
+            col = {d: k for k, d in enumerate(devs)}
+            # NaN marks a device some member lacks; any NaN (or an unknown device) takes the
+            # object path below, which reports it exactly as the reference does
+            if all(d in col for d in self.device_ids) and not np.isnan(gcost).any():
+                cost = np.ascontiguousarray(gcost[:, [col[d] for d in self.device_ids]])
+                mem = gmem
+            else:
+                fast = None
+        if fast is None:
+            cost = np.empty((n, K), dtype=np.float64)
+            for i, nid in enumerate(self.op_ids):
+                ct = gc.node(nid).compute_time
+                for k, dev in enumerate(self.device_ids):
+                    t = ct.get(dev)
+                    if t is None:
+                        if _fill_missing is None:
+                            raise MissingCostError(nid, dev)
+                        t = _fill_missing
+                    cost[i, k] = t
+            if np.isnan(cost).any():
+                i, k = map(int, np.argwhere(np.isnan(cost))[0])
+                raise ValueError(f"op {self.op_ids[i]} has a NaN compute time on device {self.device_ids[k]}; "
+                                 "NaN costs are not supported")
+            mem = np.asarray([gc.node(i).mem_bytes for i in self.op_ids], dtype=np.int64)
         cap = np.asarray([c.device(d).mem_bytes for d in self.device_ids], dtype=np.int64)
         bw = np.zeros((K, K), dtype=np.float64)
         for a, da in enumerate(self.device_ids):

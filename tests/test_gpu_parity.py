@@ -141,6 +141,21 @@ def test_gcof_parallel_and_ordered_paths_both_run_on_goldens():
     assert LAST_GCOF["ordered_replay"] is True  # contested consumers
 
 
+def test_gcof_output_arrays_feed_instance_like_its_objects():
+    """The coarsened graph builds its node objects lazily and hands its cost / memory
+    arrays to Instance; the Instance built from a plain copy (node objects) must hold
+    the same tables bit for bit, and the lazy nodes must equal the copy's."""
+    for w in (workloads.c1(), workloads.c2(8), workloads.c3(), workloads.c4("pcie")):
+        coarse = mp.gcof(w.raw, w.rules)
+        assert getattr(coarse, "_gcof_cost_arrays", None) is not None
+        plain = mp.CompGraph(coarse.nodes, coarse.edges)
+        assert plain == coarse and len(plain) == len(coarse)
+        mesh = mp.effective_bandwidth(w.cluster)
+        with mp.Instance(coarse, w.cluster, mesh) as a, mp.Instance(plain, w.cluster, mesh) as b:
+            for x, y in zip(a._arrays, b._arrays):
+                assert x.dtype == y.dtype and np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
 def test_gcof_rejects_cycles_and_is_idempotent():
     rules = workloads.table_rules()
     cyc = mp.CompGraph([mp.OpNode(1, "conv", 1, {0: 1.0}), mp.OpNode(2, "bn", 1, {0: 1.0})],
