@@ -382,13 +382,13 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             int np = 0;  // predicated loads: only an active lane's own consumer is read
             double cur = 0.0;
             uint32_t ct = 0;
-            if (act && multi) {
+            if (op_upd && multi) {  // a flow entering the ready set reads no consumer state
                 np = static_cast<int>(m_np[kc]) - 1;
                 cur = m_est[kc];
                 ct = m_tie[kc];
             }
             const bool up = end > cur;
-            const double ej = multi ? (up ? end : cur) : end;
+            const double ej = up ? end : cur;  // cur = +0.0 without state, end >= +0.0
             const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
             const uint32_t tie_j = multi ? tie_new : tj;
             if (op_upd && multi) {
@@ -402,7 +402,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const unsigned bal = __ballot_sync(kFull, ins);
             const int pos = nready + __popc(bal & below);
             if (ins && pos < rcap) {
-                rdy[pos] = make_entry(flow_ins ? end : ej, flow_ins ? fdur + rj : rj, flow_ins ? fdur : odur,
+                // est: ej == end for an entering flow (no state read); rank: fdur is +0.0
+                // unless a flow enters and +0.0 + rj == rj (rj >= +0.0)
+                rdy[pos] = make_entry(ej, fdur + rj, flow_ins ? fdur : odur,
                                       flow_ins ? fmeta
                                                : (static_cast<uint32_t>(j) | (static_cast<uint32_t>(dj) << 20) | (RZ << 26)),
                                       flow_ins ? pid : tie_j);
