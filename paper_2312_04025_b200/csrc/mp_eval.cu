@@ -274,8 +274,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             const uint32_t tie = static_cast<uint32_t>(dbits(h1.y) >> 32);
             const unsigned long long es = dbits(h0.x);
             const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
-            const unsigned long long c1 = dbits(clk[i1 <= WS ? i1 : RZ]);
-            const unsigned long long c2 = dbits(clk[i2 <= WS ? i2 : RZ]);
+            // (idle lanes hold a zero meta: slots 0; entries always name slots <= RZ)
+            const unsigned long long c1 = dbits(clk[i1]);
+            const unsigned long long c2 = dbits(clk[i2]);
             unsigned long long e = es > c1 ? es : c1;
             e = e > c2 ? e : c2;
             const unsigned long long r = dbits(h0.y);
