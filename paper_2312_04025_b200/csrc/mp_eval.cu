@@ -258,7 +258,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     while (__any_sync(kFull, !done)) {
         // -- local minimum over this lane's slice of the ready set (branch-free) ---
         const int maxr = __reduce_max_sync(kFull, done ? 0 : nready);
-        unsigned long long be = ~0ULL, br = 0ULL;
+        // keys compare as fp64 (DSETP on the FP64 pipe, one instruction per relation; all
+        // times are finite and >= +0.0)
+        double be = kInf, br = -1.0;
         uint32_t bi = 0xffffffffu, bmeta = 0;
         double bdur = 0.0;
         int bs = -1;
@@ -272,17 +274,17 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             }
             const uint32_t m = static_cast<uint32_t>(dbits(h1.y));
             const uint32_t tie = static_cast<uint32_t>(dbits(h1.y) >> 32);
-            const unsigned long long es = dbits(h0.x);
+            const double es = h0.x;
             const uint32_t i1 = (m >> 20) & 63u, i2 = m >> 26;
             // (idle lanes hold a zero meta: slots 0; entries always name slots <= RZ)
-            const unsigned long long c1 = dbits(clk[i1]);
-            const unsigned long long c2 = dbits(clk[i2]);
-            unsigned long long e = es > c1 ? es : c1;
+            const double c1 = clk[i1];
+            const double c2 = clk[i2];
+            double e = es > c1 ? es : c1;
             e = e > c2 ? e : c2;
-            const unsigned long long r = dbits(h0.y);
+            const double r = h0.y;
             const uint32_t id = (COLO && e == es) ? tie : (m & MP_NODE_MASK);
             const double du = h1.x;
-            const bool take = valid & key_less_nb(e, r, id, be, br, bi);
+            const bool take = valid & ((e < be) | ((e == be) & ((r > br) | ((r == br) & (id < bi)))));
             be = take ? e : be;
             br = take ? r : br;
             bi = take ? id : bi;
@@ -297,10 +299,10 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) {
             if (o >= maxr) continue;
-            const unsigned long long e2 = __shfl_xor_sync(kFull, be, o, G);
-            const unsigned long long r2 = __shfl_xor_sync(kFull, br, o, G);
+            const double e2 = __shfl_xor_sync(kFull, be, o, G);
+            const double r2 = __shfl_xor_sync(kFull, br, o, G);
             const uint32_t i2 = __shfl_xor_sync(kFull, bi, o, G);
-            const bool take = key_less_nb(e2, r2, i2, be, br, bi);
+            const bool take = (e2 < be) | ((e2 == be) & ((r2 > br) | ((r2 == br) & (i2 < bi))));
             be = take ? e2 : be;
             br = take ? r2 : br;
             bi = take ? i2 : bi;
@@ -324,7 +326,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         nready = done ? nready : last;
 
         // -- commit (solver.py:130-138): start = e, end = e + dur ----------------
-        const double E = bitsd(be);
+        const double E = be;
         const double end = E + wdur;
         const int node = static_cast<int>(wmeta & MP_NODE_MASK);
         const uint32_t r1 = (wmeta >> 20) & 63u, r2 = wmeta >> 26;
