@@ -261,9 +261,14 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         // keys compare as fp64 (DSETP on the FP64 pipe, one instruction per relation; all
         // times are finite and >= +0.0)
         double be = kInf, br = -1.0;
-        uint32_t bi = 0xffffffffu, bmeta = 0;
-        double bdur = 0.0;
+        uint32_t bi = 0xffffffffu;
         int bs = -1;
+        // G <= 16: the winner's meta and duration are re-read from its slot after the
+        // butterfly (three selects fewer per scanned entry); 32-lane groups (the off-chip
+        // re-run of overflowed rows, the widest graphs) carry them through the scan
+        constexpr bool kReread = G <= 16;
+        uint32_t bmeta = 0;
+        double bdur = 0.0;
         for (int s0 = 0; s0 < maxr; s0 += G) {
             const int s = s0 + gl;
             const bool valid = !done && s < nready;
@@ -283,14 +288,15 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             e = e > c2 ? e : c2;
             const double r = h0.y;
             const uint32_t id = (COLO && e == es) ? tie : (m & MP_NODE_MASK);
-            const double du = h1.x;
             const bool take = valid & ((e < be) | ((e == be) & ((r > br) | ((r == br) & (id < bi)))));
             be = take ? e : be;
             br = take ? r : br;
             bi = take ? id : bi;
-            bmeta = take ? m : bmeta;
-            bdur = take ? du : bdur;
             bs = take ? s : bs;
+            if constexpr (!kReread) {
+                bmeta = take ? m : bmeta;
+                bdur = take ? h1.x : bdur;
+            }
         }
         const uint32_t mine = bi;
         // -- G-lane butterfly: every lane ends with its group's minimum.  Entries
@@ -311,8 +317,10 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         const bool owner = !done && bs >= 0 && mine == bi;
         const unsigned own = __ballot_sync(kFull, owner) & gbits;
         const int src_lane = own ? (__ffs(own) - 1) : lane;
-        const uint32_t wmeta = __shfl_sync(kFull, bmeta, src_lane);
-        const double wdur = __shfl_sync(kFull, bdur, src_lane);
+        double2 wh = make_double2(bdur, bitsd(bmeta));  // {duration, meta | tie} of the winner's slot
+        if (kReread && owner) wh = reinterpret_cast<const double2 *>(rdy + bs)[1];
+        const uint32_t wmeta = __shfl_sync(kFull, static_cast<uint32_t>(dbits(wh.y)), src_lane);
+        const double wdur = __shfl_sync(kFull, wh.x, src_lane);
         be = __shfl_sync(kFull, be, src_lane);  // lanes >= maxr skipped butterfly rounds
         const int last = nready - 1;
         __syncwarp();  // every lane's scan reads precede the refill of the hole
