@@ -14,7 +14,9 @@
  *    message.  The Python host (paper_2312_04025_b200/_native.py) maps codes onto
  *    the reference exception tree (pkg/src/opplace/errors.py).
  *  - No C++ or torch types cross the boundary: plain pointers, sizes, and an
- *    opaque cudaStream_t passed as void* (NULL = the library's own stream).
+ *    opaque cudaStream_t passed as void* (NULL = the library's own stream, which is
+ *    ordered with the legacy default stream like any blocking stream: work a caller
+ *    enqueued on stream 0 before the call completes before the call's kernels read it).
  *  - Buffers are caller-owned.  Unless MP_DEVICE_PTRS is set in `flags`, array
  *    arguments are HOST pointers and the library stages them through its own
  *    pinned/device buffers (host<->device copies happen inside the call).

@@ -755,7 +755,10 @@ int32_t mp_instance_create(const mp_problem *prob, int32_t device, mp_instance *
                                 cudaGetErrorString(e_), __FILE__, __LINE__));                          \
     } while (0)
 
-    MP_CUDA_I(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+    // the instance's own stream (stream argument NULL) is a BLOCKING stream: it is ordered
+    // with the legacy default stream, so a caller that fills device rows on stream 0 and
+    // passes stream 0 (= NULL) gets stream order, not a race
+    MP_CUDA_I(cudaStreamCreate(&I->stream));
     MP_CUDA_I(cudaStreamCreateWithFlags(&I->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         MP_CUDA_I(cudaEventCreateWithFlags(&I->ev_copy[k], cudaEventDisableTiming));

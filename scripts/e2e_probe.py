@@ -95,6 +95,15 @@ def gpu_span(label, fn, n=5):
 
 gpu_span("device ptrs", lambda: call(False))
 gpu_span("host (streamed)", lambda: call(True))
+
+
+def fresh_then_call():
+    d.copy_(h, non_blocking=True)  # rows just written by DMA, then the kernel reads them
+    call(False)
+
+
+gpu_span("device ptrs, rows freshly copied (copy + call)", fresh_then_call)
+gpu_span("copy only", lambda: d.copy_(h, non_blocking=True))
 for _ in range(2):
     timed("device ptrs", lambda: call(False))
     timed("device ptrs + 8 MB makespan read-back", dev_with_readback)

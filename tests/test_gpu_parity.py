@@ -360,6 +360,38 @@ def test_device_pointer_path_and_chunking():
         assert np.array_equal(bits(d_ms.cpu().numpy()), bits(host_ms))
 
 
+def test_device_pointer_call_is_ordered_after_default_stream_work():
+    """Rows filled on the legacy default stream by an asynchronous copy right before a
+    device-pointer call with stream NULL (= torch's stream 0) must be the rows the call
+    evaluates: the library's own stream is ordered with the default stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2312_04025_b200 import _native as N
+
+    w = workloads.c2(8)
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        P = 1 << 18
+        A = workloads.placements(2, P, inst.n_ops, inst.K)
+        B = workloads.placements(3, P, inst.n_ops, inst.K)
+        want = mp.evaluate_batch(inst, B)
+        hA, hB = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+        d = torch.empty_like(hA, device="cuda")
+        dm = torch.empty(P, dtype=torch.float64, device="cuda")
+        err = N.mp_error()
+        for _ in range(3):
+            d.copy_(hA)
+            torch.cuda.synchronize()
+            d.copy_(hB, non_blocking=True)  # still in flight when the call is enqueued
+            code = inst._lib.mp_evaluate_batch(inst.handle, C.c_void_p(d.data_ptr()), P, C.c_void_p(dm.data_ptr()),
+                                               None, None, None, N.MP_DEVICE_PTRS, None, C.byref(err))
+            N.check(code, err)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(dm.cpu().numpy()), bits(want))
+
+
 # ---- local search (K5): every reported placement re-verifies bit-exactly -----------------
 def test_local_search_reverifies_and_is_deterministic(oracle_mod):
     w = workloads.c2(4)
