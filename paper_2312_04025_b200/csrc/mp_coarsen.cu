@@ -124,6 +124,8 @@ struct DfsState {
     int *seq;       // [V*Lmax] by group id: the sequence (valid when len <= Lmax)
     int *tag;       // [V] by group id
     int2 *obt;      // [V] by group id: out-edge range [obeg[tail], obeg[tail+1]) of the group's tail
+    int2 *osc;      // [V] by group id (global-memory replay only): the tail's first two input
+                    //     successors (-1 = none), so out-degree <= 2 needs no odst gather
     unsigned char *visited;  // [V] by group id
     unsigned char *vl;       // [V] (large graphs, shared memory) visited << 7 | length, replacing
                              //     `visited` and `len` inside the DFS (VL variant of dfs_run)
@@ -141,10 +143,14 @@ __device__ __forceinline__ int dfs_len(const DfsState &s, int g) {
 
 // Initial per-node state: singleton groups with the node's own type sequence.
 __global__ void k_init_nodes(int V, int Lmax, const int *seq_beg, const int *seq_types, const int *tag_in, Trie t,
-                             const int *obeg, DfsState s) {
+                             const int *obeg, const int *odst, DfsState s) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         s.where[v] = v;
         s.obt[v] = make_int2(obeg[v], obeg[v + 1]);
+        if (s.osc) {
+            const int b = obeg[v], n = obeg[v + 1] - b;
+            s.osc[v] = make_int2(n > 0 ? odst[b] : -1, n > 1 ? odst[b + 1] : -1);
+        }
         s.next[v] = -1;
         s.head[v] = v;
         s.tail[v] = v;
@@ -350,13 +356,45 @@ struct OutSet {
     bool lead;      // this lane represents w
     bool vis;       // visited[w] (leaders)
     bool wide;      // out-degree > 32: the set is in buf[0..n) (scalar form)
+    bool fast;      // VL, out-degree <= 2: every lane holds the (at most two) groups
+    int f0, f1;     // fast: the distinct out groups (-1 = none), f0 set first
+    bool v0, v1;    // fast: their visited flags
 };
 
 template <bool VL>
-__device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *odst, int2 ob, int self, int *buf) {
+__device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *odst, int2 ob, int2 oc, int self,
+                                                  int *buf) {
     const int lane = threadIdx.x & 31;
     OutSet o;
+    o.fast = false;
     o.wide = ob.y - ob.x > 32;
+    if (VL && ob.y - ob.x <= 2) {
+        // scalar form without warp collectives: every lane loads the same one or two
+        // successors' groups and visited / length bytes (broadcast loads)
+        const int deg = ob.y - ob.x;
+        int w0 = deg > 0 ? s.where[oc.x] : -1;
+        int w1 = deg > 1 ? s.where[oc.y] : -1;
+        if (w0 == self) w0 = -1;
+        if (w1 == self || w1 == w0) w1 = -1;
+        if (w0 < 0) {
+            w0 = w1;
+            w1 = -1;
+        }
+        const unsigned a0 = w0 >= 0 ? s.vl[w0] : 0x80u, a1 = w1 >= 0 ? s.vl[w1] : 0x80u;
+        o.fast = true;
+        o.wide = false;
+        o.n = (w0 >= 0 ? 1 : 0) + (w1 >= 0 ? 1 : 0);
+        o.one = w0;
+        o.one_len = static_cast<int>(a0 & 0x7fu);
+        o.f0 = w0;
+        o.f1 = w1;
+        o.v0 = (a0 >> 7) != 0;
+        o.v1 = (a1 >> 7) != 0;
+        o.w = -1;
+        o.lead = false;
+        o.vis = true;
+        return o;
+    }
     if (o.wide) {
         o.n = out_groups(s, odst, ob, self, buf);
         o.one = buf[0];
@@ -367,8 +405,11 @@ __device__ __forceinline__ OutSet out_groups_warp(const DfsState &s, const int *
     }
     int w = -1, lw = 0;
     bool vis = true;
-    if (ob.x + lane < ob.y) {
-        const int x = s.where[odst[ob.x + lane]];
+    const int deg = ob.y - ob.x;
+    if (lane < deg) {
+        // VL: out-degree <= 2 reads the successors from the group's record (no odst gather)
+        const int y = (VL && deg <= 2) ? (lane == 0 ? oc.x : oc.y) : odst[ob.x + lane];
+        const int x = s.where[y];
         if constexpr (VL) {  // x is a live group id even when it is `self`
             const unsigned v = s.vl[x];
             vis = (v >> 7) != 0;
@@ -412,6 +453,10 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
         stack[sp++] = src;
         __syncwarp();
         int top = -1;  // the group just pushed on top of the stack, if any
+        // VL: the last group record loaded ahead (the first successor of the last
+        // group walked); reused when that group is popped next
+        int sv_id = -1, sv_h = 0, sv_t = 0, sv_st = 0, sv_seq = 0;
+        int2 sv_ob = make_int2(0, 0), sv_oc = make_int2(-1, -1);
         while (sp > 0) {
             // a group pushed by the previous step is still a live group id (nothing
             // merged since), so where[top] == top: skip the stack and where loads
@@ -423,22 +468,75 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
             } else {
                 cur = s.where[stack[--sp]];
             }
-            // independent loads of cur's record, issued together
+            // independent loads of cur's record (its sequence held lane q = element q),
+            // issued together
             const bool seen = dfs_visited<VL>(s, cur);
-            int2 ob = s.obt[cur];
-            int st_cur = s.state[cur];
             int len_cur = dfs_len<VL>(s, cur);
+            int2 ob, oc = make_int2(-1, -1);
+            int st_cur, h_cur, t_cur, seq_cur;
+            if (VL && cur == sv_id) {  // nothing rewrote its record since it was loaded
+                ob = sv_ob;
+                oc = sv_oc;
+                st_cur = sv_st;
+                h_cur = sv_h;
+                t_cur = sv_t;
+                seq_cur = sv_seq;
+            } else {
+                ob = s.obt[cur];
+                if constexpr (VL) oc = s.osc[cur];
+                st_cur = s.state[cur];
+                h_cur = s.head[cur];
+                t_cur = s.tail[cur];
+                seq_cur = lane < Lmax ? s.seq[static_cast<size_t>(cur) * Lmax + lane] : 0;
+            }
             if (seen) continue;
             OutSet os;
             for (;;) {
+                // VL: the record of the first successor's group, loaded beside the where
+                // gather and used when that successor is the one out group and still its
+                // group's id (the common chain step: one dependent round trip, not two)
+                const int spec = oc.x;
+                int h_sp = 0, t_sp = 0, sn_sp = 0;
+                int2 ob_sp = make_int2(0, 0), oc_sp = make_int2(-1, -1);
+                if (VL && spec >= 0) {
+                    h_sp = s.head[spec];
+                    t_sp = s.tail[spec];
+                    ob_sp = s.obt[spec];
+                    oc_sp = s.osc[spec];
+                    sn_sp = lane < Lmax ? s.seq[static_cast<size_t>(spec) * Lmax + lane] : 0;
+                    sv_st = s.state[spec];
+                }
+                if constexpr (VL) {
+                    sv_id = spec;
+                    sv_h = h_sp;
+                    sv_t = t_sp;
+                    sv_ob = ob_sp;
+                    sv_oc = oc_sp;
+                    sv_seq = sn_sp;
+                }
                 // |out[cur]| == 1 ?  (fusion.py:291-294)
-                os = out_groups_warp<VL>(s, odst, ob, cur, buf);
+                os = out_groups_warp<VL>(s, odst, ob, oc, cur, buf);
                 if (os.n != 1) break;
                 const int nxt = os.one;
+                int h_nxt, t_nxt, sn_all;
+                int2 ob_nxt, oc_nxt = make_int2(-1, -1);
+                if (VL && nxt == spec) {
+                    h_nxt = h_sp;
+                    t_nxt = t_sp;
+                    ob_nxt = ob_sp;
+                    oc_nxt = oc_sp;
+                    sn_all = sn_sp;
+                } else {
+                    h_nxt = s.head[nxt];
+                    t_nxt = s.tail[nxt];
+                    ob_nxt = s.obt[nxt];
+                    if constexpr (VL) oc_nxt = s.osc[nxt];
+                    sn_all = lane < Lmax ? s.seq[static_cast<size_t>(nxt) * Lmax + lane] : 0;
+                }
                 // _match_seqs(seqs[cur], seqs[nxt]) (fusion.py:93-104) via the trie
                 const int ln = os.one_len;
                 if (st_cur < 0 || ln > Lmax || len_cur + ln > Lmax) break;
-                const int sn = lane < ln ? s.seq[static_cast<size_t>(nxt) * Lmax + lane] : 0;  // nxt's types
+                const int sn = lane < ln ? sn_all : 0;  // nxt's types
                 int st = st_cur;
                 for (int q = 0; q < ln; ++q) st = trie_step(t, st, __shfl_sync(0xffffffffu, sn, q));
                 if (st < 0) break;
@@ -452,9 +550,7 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 const int lc = len_cur;
                 const int L2 = lc + ln;  // <= Lmax <= 30: lane q moves element q
                 const int from_n = __shfl_sync(0xffffffffu, sn, (lane - lc) & 31);
-                const int sv = lane < lc ? s.seq[static_cast<size_t>(cur) * Lmax + lane] : from_n;
-                const int h_cur = s.head[cur], t_cur = s.tail[cur], h_nxt = s.head[nxt], t_nxt = s.tail[nxt];
-                const int2 ob_nxt = s.obt[nxt];
+                const int sv = lane < lc ? seq_cur : from_n;
                 __syncwarp();  // every lane has read cur's / nxt's records before any lane rewrites them
                 // rename the members of the group whose id disappears
                 if (nw == cur) {
@@ -472,6 +568,7 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.head[nw] = h_cur;
                 s.tail[nw] = t_nxt;
                 s.obt[nw] = ob_nxt;
+                if constexpr (VL) s.osc[nw] = oc_nxt;
                 if constexpr (VL) {  // read-modify-write: one lane (the __syncwarp below publishes it)
                     if (lane == 0) s.vl[nw] = static_cast<unsigned char>((s.vl[nw] & 0x80u) | static_cast<unsigned>(L2));
                 } else {
@@ -484,8 +581,11 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.tag[nw] = kind == 2 ? kTagBound : kTagFused;
                 cur = nw;
                 ob = ob_nxt;
+                oc = oc_nxt;
                 st_cur = st;
                 len_cur = L2;
+                t_cur = t_nxt;  // (the head stays h_cur)
+                seq_cur = sv;
             }
             if constexpr (VL) {
                 if (lane == 0) s.vl[cur] = static_cast<unsigned char>(s.vl[cur] | 0x80u);
@@ -494,6 +594,23 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
                 s.visited[cur] = 1;
             }
             // push unvisited out groups in descending id (fusion.py:301-303)
+            if (VL && os.fast) {  // every lane writes the same values
+                const bool p0 = os.f0 >= 0 && !os.v0, p1 = os.f1 >= 0 && !os.v1;
+                if (p0 && p1) {
+                    const int lo = os.f0 < os.f1 ? os.f0 : os.f1, hi = os.f0 < os.f1 ? os.f1 : os.f0;
+                    stack[sp] = hi;
+                    stack[sp + 1] = lo;
+                    sp += 2;
+                    top = lo;
+                } else if (p0 || p1) {
+                    const int x = p0 ? os.f0 : os.f1;
+                    stack[sp] = x;
+                    sp += 1;
+                    top = x;
+                }
+                __syncwarp();
+                continue;
+            }
             if (!os.wide) {
                 // position of a pushed group = number of pushed groups above it
                 const bool push = os.lead && !os.vis;
@@ -525,21 +642,35 @@ __device__ void dfs_run(int V, int Lmax, const int *indeg, const int *obeg, cons
     }
 }
 
-__global__ void k_dfs(int V, int Lmax, const int *indeg, const int *obeg, const int *odst, Trie t, DfsState s,
-                      int *stack, int *buf,
-                      int use_vl, const int *hazard) {
+__global__ void k_dfs(int V, int Lmax, int TN, const int *indeg, const int *obeg, const int *odst, Trie t,
+                      DfsState s, int *stack, int *buf, int use_vl, int trie_sm, const int *hazard) {
     if (threadIdx.x >= 32 || blockIdx.x != 0 || *hazard == 0) return;  // hazard-free: k_chains resolved it
     if (!use_vl) {
         dfs_run<false>(V, Lmax, indeg, obeg, odst, t, s, stack, buf);
         return;
     }
     // visited flags and lengths (<= Lmax + 1 <= 31) in one shared-memory byte per group
-    extern __shared__ unsigned char vl_sm[];
+    extern __shared__ __align__(16) unsigned char vl_sm[];
     DfsState q = s;
     q.vl = vl_sm;
     for (int i = threadIdx.x; i < V; i += 32) vl_sm[i] = static_cast<unsigned char>(s.len[i]);
+    // the rule trie behind the bytes when it fits: every match step walks it
+    Trie ts = t;
+    if (trie_sm) {
+        int *tb = reinterpret_cast<int *>(vl_sm + ((V + 15) & ~15));
+        ts.child = tb;
+        ts.sibling = tb + TN;
+        ts.type = tb + 2 * TN;
+        ts.flags = tb + 3 * TN;
+        for (int i = threadIdx.x; i < TN; i += 32) {
+            ts.child[i] = t.child[i];
+            ts.sibling[i] = t.sibling[i];
+            ts.type[i] = t.type[i];
+            ts.flags[i] = t.flags[i];
+        }
+    }
     __syncwarp();
-    dfs_run<true>(V, Lmax, indeg, obeg, odst, t, q, stack, buf);
+    dfs_run<true>(V, Lmax, indeg, obeg, odst, ts, q, stack, buf);
     // len is read again only by this kernel; visited not at all after it
 }
 
@@ -954,7 +1085,7 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
                                    std::max(E, 1));
     const size_t tmpb = std::max(std::max(tmp_bytes, t2), std::max(t3, t4)) + 256;
     size_t need = up_used + tmpb + 96 * 512;
-    need += 4ULL * ((V + 1ULL) * 44 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
+    need += 4ULL * ((V + 1ULL) * 46 + 8ULL * E + 4ULL * TN + static_cast<size_t>(V) * Lmax + 64);
     need += 8ULL * (4ULL * V + 2ULL * V * D + 10ULL * E + O + 64);
     if (cx.dev_cap < need) {
         if (cx.dev) cudaFree(cx.dev);
@@ -1064,12 +1195,13 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
         s.seq = ar.take<int>(static_cast<size_t>(V) * Lmax);
         s.tag = ar.take<int>(V);
         s.obt = ar.take<int2>(V);
+        s.osc = dfs_in_smem ? nullptr : ar.take<int2>(V);
         s.visited = ar.take<unsigned char>(V);
         int *stack = ar.take<int>(stack_cap), *buf = ar.take<int>(stack_cap);
         int *ntrie = ar.take<int>(4);
         k_build_trie<<<1, 32, 0, st>>>(R, d_rbeg, d_rt, trie, ntrie);
         ++g_mp_launches;
-        k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, obeg, s);
+        k_init_nodes<<<grid, 256, 0, st>>>(V, Lmax, d_seq_beg, d_seq, d_tag, trie, obeg, odst, s);
         ++g_mp_launches;
         // K1p: the hazard test and, on hazard-free graphs, the parallel resolution;
         // exactly one of k_chains / the DFS replay does work (the flag stays on the device)
@@ -1099,12 +1231,15 @@ extern "C" int32_t mp_coarsen(const mp_coarsen_input *in, int32_t device, mp_coa
             // per group) sit in shared memory when they fit, the rest of the SM's unified
             // L1 caches the state
             const bool use_vl = static_cast<size_t>(V) <= static_cast<size_t>(MP_SMEM_DYN_MAX);
+            const size_t trie_b = ((static_cast<size_t>(V) + 15) & ~static_cast<size_t>(15)) + 16ULL * TN;
+            const bool trie_sm = use_vl && trie_b <= static_cast<size_t>(MP_SMEM_DYN_MAX);
             if (!cx.dfs_attr) {
                 CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_dfs),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, MP_SMEM_DYN_MAX));
                 cx.dfs_attr = true;
             }
-            k_dfs<<<1, 32, use_vl ? V : 0, st>>>(V, Lmax, indeg, obeg, odst, trie, s, stack, buf, use_vl ? 1 : 0, hazard);
+            k_dfs<<<1, 32, trie_sm ? trie_b : (use_vl ? V : 0), st>>>(V, Lmax, TN, indeg, obeg, odst, trie, s, stack, buf,
+                                                                     use_vl ? 1 : 0, trie_sm ? 1 : 0, hazard);
         }
         ++g_mp_launches;
 
