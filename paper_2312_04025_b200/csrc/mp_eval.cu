@@ -1684,7 +1684,19 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         const int maxc = __reduce_max_sync(kFull, cnt);
         // successors' loads are issued before the duration, removal and commit
         // (none of which writes what they read)
-        constexpr int SU = 2;
+#ifndef MP_TPP2_COMPACT
+#define MP_TPP2_COMPACT -1
+#endif
+        // COMPACT: every lane handles its winner's first SU successors itself; the rest (out-flows
+        // SU+1.. of multi-output ops) are dealt to the warp's lanes as one work list.  Default
+        // (-1): on for the divided-duration kernels (many payload classes, wide ready sets: C1
+        // +4.7 %), off with the duration table (C2 / C4: -4 %; profiles/r02/ab_compact.txt)
+        constexpr bool CMP = MP_TPP2_COMPACT == 1 || (MP_TPP2_COMPACT == -1 && !TAB);
+#ifdef MP_TPP2_SU
+        constexpr int SU = MP_TPP2_SU;
+#else
+        constexpr int SU = CMP ? 1 : 2;
+#endif
         int j_[SU], dj_[SU];
         uint32_t pid_[SU], k_[SU], cb_[SU];
         unsigned long long tn_[SU];
@@ -1729,6 +1741,86 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
             }
         };
         if (maxc > 0) phase_a(0);
+        // COMPACT work list (out-flows SU+1.. of multi-output winners, dealt to the warp's lanes):
+        // lane o owns items [excl_o, incl_o); round 0's loads are issued here, beside the
+        // lanes' own first successors, before the duration / removal / commit
+        struct RemItem {
+            bool valid, multi, cross, via_colo, flow_ins, op_upd;
+            int o, exo, otid, j, dj;
+            uint32_t pid, k, cb;
+            long long glo;
+            double pay, rj, cur;
+            unsigned long long tn;
+        };
+        int c_incl = 0, c_excl = 0, c_total = 0;
+        const int c_ln = v.tid & 31;
+        auto rem_load = [&](int base) -> RemItem {
+            RemItem it;
+            const int x = base + c_ln;
+            it.valid = x < c_total;
+            int o = 0;  // owner: the first lane whose inclusive count exceeds x
+#pragma unroll
+            for (int b = 16; b > 0; b >>= 1) o += (__shfl_sync(kFull, c_incl, o + b - 1) <= x) ? b : 0;
+            o = o > 31 ? 31 : o;
+            it.o = o;
+            it.exo = __shfl_sync(kFull, c_excl, o);
+            const int obo = __shfl_sync(kFull, ob, o);
+            const int dO = __shfl_sync(kFull, d, o);
+            it.otid = (v.tid & ~31) + o;
+            it.glo = static_cast<long long>(blockIdx.x) * T + it.otid;
+            const int qq = it.valid ? obo + (x - it.exo) + SU : 0;
+            unsigned long long rb;
+            it.pay = 0.0;
+            if constexpr (TAB) {
+                rb = T_rec8[qq];
+            } else {
+                const double2 rec = T_rec[qq];
+                rb = dbits(rec.x);
+                it.pay = rec.y;
+            }
+            it.j = static_cast<int>(static_cast<uint32_t>(rb) & MP_NODE_MASK);
+            it.pid = static_cast<uint32_t>(rb >> 32);
+            it.cb = static_cast<uint32_t>(rb) >> MP_NODE_BITS;
+            const int jj = it.j;
+            if constexpr (R3) {
+                const int w = div10(jj);
+                it.dj = static_cast<int>((reinterpret_cast<const uint32_t *>(v.rowt)[w * T + it.otid] >> (3 * (jj - 10 * w))) & 7u);
+            } else {
+                it.dj = (v.rowt[(jj >> 1) * T + it.otid] >> ((jj & 1) << 2)) & 15;
+            }
+            const double *rp = reinterpret_cast<const double *>(
+                a.gstate + it.glo * 8 + static_cast<unsigned long long>(static_cast<unsigned>(jj) * L8));
+            it.rj = it.valid ? (GC ? __ldcg(rp) : *rp) : 0.0;
+            it.k = T_mi[jj];
+            it.multi = it.k != MP_NONE;
+            it.cross = it.dj != dO;
+            it.via_colo = COLO & !it.cross;
+            it.flow_ins = it.valid & !it.via_colo;
+            it.op_upd = it.valid & it.via_colo;
+            it.cur = 0.0;
+            it.tn = 1ULL << 32;
+            if (it.op_upd & it.multi) {
+                const double2 *mp = reinterpret_cast<const double2 *>(
+                    a.gstate + static_cast<long long>(n_ops) * v.L * 8 + it.glo * 16 + static_cast<unsigned long long>(it.k * L16));
+                const double2 ms2 = GC ? __ldcg(mp) : *mp;
+                it.cur = ms2.x;
+                it.tn = dbits(ms2.y);
+            }
+            return it;
+        };
+        RemItem it0;
+        if (CMP && maxc > SU) {  // warp-uniform: some lane's winner is an op with >= 2 out-flows
+            const int rem = cnt > SU ? cnt - SU : 0;
+            c_incl = rem;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, c_incl, o);
+                c_incl += (c_ln >= o) ? y : 0;
+            }
+            c_excl = c_incl - rem;
+            c_total = __shfl_sync(kFull, c_incl, 31);
+            it0 = rem_load(0);
+        }
         // the winner's duration: op cost, payload / bw for a crossing flow, 0 for a
         // co-located flow dispatched as a node (colo off)
         double bd = 0.0;
@@ -1769,11 +1861,12 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
         }
         ms = (!done & (node < n_ops) & (end > ms)) ? end : ms;
         // -- successors (solver.py:140-145): op -> its out-flows, flow -> its consumer
-        for (int t0 = 0; t0 < maxc; t0 += SU) {
+        const int maxl = CMP ? (maxc < SU ? maxc : SU) : maxc;
+        for (int t0 = 0; t0 < maxl; t0 += SU) {
             if (t0 > 0) phase_a(t0);
 #pragma unroll
             for (int u = 0; u < SU; ++u) {
-                if (t0 + u >= maxc) break;
+                if (t0 + u >= maxl) break;
                 const int j = j_[u], dj = dj_[u];
                 const uint32_t pid = pid_[u];
                 const bool act = act_[u];
@@ -1819,6 +1912,64 @@ __device__ __forceinline__ TppResult tpp2_eval(const TppView &v, const EvalArgs 
                        // colo mode: every end > 0 (all durations > 0), so up holds for a
                        // consumer without multi-input state and tie_new == tj
                        (flow_ins ? fhi : (((COLO | multi) ? tie_new : tj) | (op_r2(static_cast<uint32_t>(dj)) << 26))));
+            }
+        }
+        if constexpr (CMP) {
+            if (maxc > SU) {
+                __syncwarp();  // the owners' first-successor stores precede the dealt items
+                for (int base = 0; base < c_total; base += 32) {
+                    const RemItem it = base == 0 ? it0 : rem_load(base);
+                    const int dO = __shfl_sync(kFull, d, it.o);
+                    const double endO = __shfl_sync(kFull, end, it.o);
+                    const int nrO = __shfl_sync(kFull, nr, it.o);
+                    double fdur = 0.0;
+                    if constexpr (TAB) {
+                        if (it.valid & it.cross) fdur = T_fdur[it.cb + dO * K + it.dj];
+                    } else {
+                        const int bi2 = it.cross ? dO * K + it.dj : 0;
+                        fdur = it.cross ? div_bw(it.pay, T_bw[bi2], T_rbw[bi2], fast) : 0.0;
+                    }
+                    const bool chan = COLO | it.cross;
+                    const uint32_t flo = it.pid | ((chan ? static_cast<uint32_t>(K + dO) : RZ) << 26);
+                    const uint32_t fhi = it.pid | ((chan ? static_cast<uint32_t>(2 * K + it.dj) : RZ) << 26);
+                    const uint32_t ct = static_cast<uint32_t>(it.tn);
+                    const uint32_t np = static_cast<uint32_t>(it.tn >> 32) - 1u;
+                    const uint32_t tj = it.via_colo ? it.pid : static_cast<uint32_t>(it.j);
+                    const bool up = endO > it.cur;
+                    const double ej = up ? endO : it.cur;
+                    const uint32_t tie_new = up ? tj : ((it.via_colo & (endO == it.cur) & (it.pid > ct)) ? it.pid : ct);
+                    if (it.op_upd & it.multi)
+                        *reinterpret_cast<double2 *>(a.gstate + static_cast<long long>(n_ops) * v.L * 8 + it.glo * 16 +
+                                                     static_cast<unsigned long long>(it.k * L16)) =
+                            make_double2(ej, bitsd(static_cast<unsigned long long>(tie_new) |
+                                                   (static_cast<unsigned long long>(np) << 32)));
+                    const bool ins = it.flow_ins | (it.op_upd & (!it.multi | (np == 0u)));
+                    const unsigned bal = __ballot_sync(kFull, ins);
+                    // position among this owner's inserts of the round (its items are contiguous)
+                    const int lo_o = it.exo - base > 0 ? it.exo - base : 0;
+                    const unsigned below = bal & ((1u << c_ln) - 1u) & ~((1u << lo_o) - 1u);
+                    const int pos = nrO + __popc(below);
+                    if (ins & (pos < cap)) {
+                        unsigned long long *pp = v.rE + it.otid + static_cast<size_t>(pos) * T;
+                        pp[0] = dbits(ej);
+                        pp[DR] = dbits(fdur + it.rj);
+                        const uint32_t mlo32 =
+                            it.flow_ins ? flo : (static_cast<uint32_t>(it.j) | (static_cast<uint32_t>(it.dj) << 26));
+                        const uint32_t mhi32 =
+                            it.flow_ins ? fhi
+                                        : (((COLO | it.multi) ? tie_new : tj) | (op_r2(static_cast<uint32_t>(it.dj)) << 26));
+                        pp[DM] = static_cast<unsigned long long>(mlo32) | (static_cast<unsigned long long>(mhi32) << 32);
+                    }
+                    // owner side: this lane's items in the round are lanes [lo, hi)
+                    const int lo = c_excl - base < 0 ? 0 : (c_excl - base > 32 ? 32 : c_excl - base);
+                    const int hi = c_incl - base < 0 ? 0 : (c_incl - base > 32 ? 32 : c_incl - base);
+                    const unsigned mhi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+                    const unsigned mlo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
+                    const int nins = __popc(bal & mhi & ~mlo);
+                    ovf = ovf | (nr + nins > cap);
+                    nr = (nr + nins > cap) ? cap : nr + nins;
+                }
+                __syncwarp();  // the dealt stores precede the owners' next scan
             }
         }
         done = done | ovf | (nr == 0);
