@@ -281,9 +281,9 @@ def _gcof_result(g, flat, ng, D, mbeg, members, gmem, gcost, grp_tag, esrc, edst
     if ng:
         mb = np.array(mbeg[: ng + 1], dtype=np.int64)
         mem_idx = np.array(members[: int(mb[-1])], dtype=np.int64)
-        ids = ids_in[np.minimum.reduceat(mem_idx, mb[:-1])].tolist()  # id = the smallest member id
+        ids = ids_in[np.minimum.reduceat(mem_idx, mb[:-1])]  # id = the smallest member id (int64 array)
     else:
-        mb, mem_idx, ids = np.zeros(1, np.int64), np.zeros(0, np.int64), []
+        mb, mem_idx, ids = np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
     cost = np.array(gcost, dtype=np.float64).reshape(ng, max(D, 1))
     gmem_c = np.array(gmem, dtype=np.int64)
     tag_c = np.array(grp_tag, dtype=np.int32)
