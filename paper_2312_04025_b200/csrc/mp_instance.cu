@@ -1287,6 +1287,8 @@ int evaluate_impl(mp_instance *I, const uint8_t *rows, long long n_rows, double 
             MP_CUDA(I->rows_dev[0].ensure(static_cast<size_t>(n_rows * row_bytes + 64)));
             MP_CUDA(I->out_dev[0].ensure(static_cast<size_t>(n_rows) * (8 + 1 + 4 + 8) + 64));
             MP_CUDA(I->sflag.ensure(16));
+            // one pass over all n_rows (prepare sized the overflow list for one chunk)
+            if (first_rcap(I) < I->ready_bound) MP_CUDA(I->ovf_rows.ensure(static_cast<size_t>(n_rows) * 8));
             unsigned int *flag = static_cast<unsigned int *>(I->sflag.p);
             MP_CUDA(cudaMemsetAsync(flag, 0, 8, s));
             MP_CUDA(cudaEventRecord(I->ev_used[0], s));

@@ -78,3 +78,22 @@ def test_c5_large_graphs_256_rows(oracle_mod, n):
         orc = oracle_mod.OracleInstance.from_instance(inst)
         rows = workloads.placements(w.seed, 256, inst.n_ops, inst.K)
         assert _check(inst, orc, rows) == 256
+
+
+@pytest.mark.gpu
+def test_streamed_host_batch_with_mostly_overflowing_rows():
+    """A host batch large enough to be streamed into one kernel pass (>= 16 x SMs x 512 rows)
+    whose ready sets mostly outgrow a forced two-slot capacity: the overflow list must hold
+    more than one chunk's worth of rows, and the results equal those of small batches."""
+    w = workloads.c1()
+    coarse = mp.gcof(w.raw, w.rules)
+    with mp.Instance(coarse, w.cluster, mp.effective_bandwidth(w.cluster)) as inst:
+        inst.tune(ready_cap=2)
+        n = 16 * 148 * 512 + 4096
+        rows = workloads.placements(11, n, inst.n_ops, inst.K)
+        ms, st, _, _ = mp.evaluate_batch(inst, rows, with_detail=True)
+        step = 1 << 16
+        for r0 in range(0, n, step):
+            m2, s2, _, _ = mp.evaluate_batch(inst, rows[r0:r0 + step], with_detail=True)
+            assert np.array_equal(s2, st[r0:r0 + step])
+            assert np.array_equal(bits(m2), bits(ms[r0:r0 + step])), r0
