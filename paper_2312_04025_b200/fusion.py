@@ -155,6 +155,44 @@ class _NodeArrays:
                     cost[i, dindex[k]] = float(t)
         self.cost = np.ascontiguousarray(cost)
 
+    @classmethod
+    def from_file_arrays(cls, a: dict, order: np.ndarray) -> "_NodeArrays":
+        """The same arrays from the native reader's output (file order, ``order`` =
+        ascending-id permutation), vectorised: no OpNode objects needed."""
+        na = cls.__new__(cls)
+        strs = a["strings"]
+        V = len(order)
+        sb = a["seq_beg"].astype(np.int64)
+        lens = (sb[1:] - sb[:-1])[order]
+        na.seq_beg = np.zeros(V + 1, np.int32)
+        np.cumsum(lens, out=na.seq_beg[1:])
+        total = int(na.seq_beg[-1])
+        # flattened type sequences in ascending-id node order (string-table indices)
+        starts = np.repeat(sb[:-1][order] - na.seq_beg[:-1], lens)
+        flat = a["seq"].astype(np.int64)[np.arange(total) + starts] if total else np.zeros(0, np.int64)
+        # type ids by first appearance (dict.fromkeys order of the object path)
+        uniq, first = np.unique(flat, return_index=True)
+        by_first = uniq[np.argsort(first, kind="stable")]
+        na.types = {strs[int(x)]: k for k, x in enumerate(by_first.tolist())}
+        remap = np.zeros(max(len(strs), 1), np.int32)
+        remap[by_first] = np.arange(len(by_first), dtype=np.int32)
+        na.seq = remap[flat].astype(np.int32) if total else np.zeros(0, np.int32)
+        na.tag = a["tag"].astype(np.int32)[order]  # the reader's codes are _TAG_CODE's
+        na.mem = a["mem"].astype(np.int64)[order]
+        cdev = a["ct_dev"]
+        na.devices = sorted(set(np.unique(cdev).tolist()))
+        D = len(na.devices)
+        cost = np.full((V, max(D, 1)), np.nan)
+        if len(cdev):
+            inv = np.empty(V, np.int64)
+            inv[order] = np.arange(V)
+            cb = a["ct_beg"].astype(np.int64)
+            node_of = np.repeat(inv, cb[1:] - cb[:-1])
+            col = np.searchsorted(np.asarray(na.devices, dtype=np.int64), cdev)
+            cost[node_of, col] = a["ct_val"]
+        na.cost = np.ascontiguousarray(cost)
+        return na
+
     @staticmethod
     def of(g: CompGraph) -> "_NodeArrays":
         na = getattr(g, "_gcof_node_arrays", None)

@@ -77,3 +77,40 @@ def test_other_documents_round_trip(tmp_path):
     assert dict(fileio.load_overrides(tmp_path / "o.json").entries) == dict(ov.entries)
     text = (tmp_path / "c.json").read_text()
     assert text.endswith("\n") and json.loads(text)["schema"] == 1 and '"kind": "cluster"' in text
+
+
+def test_loaded_graph_carries_gcof_arrays_without_objects(tmp_path):
+    """load_graph's GCOF input (interned type sequences, tags, memory, cost matrix) is
+    built from the native reader's arrays, nodes in any file order and with sparse device
+    costs, equal to the object path's; no OpNode is built until someone asks."""
+    import random
+
+    import numpy as np
+
+    from paper_2312_04025_b200.fusion import _NodeArrays
+
+    graphs = [graph_from(c["graph"]) for c in golden("gcof.json")[:60]]
+    graphs.append(mp.gen_synthetic(mp.GenSpec(ops=2000, width=16, density=0.5, devices=(0, 1, 2)), 7))
+    graphs.append(mp.CompGraph([mp.OpNode(5, "conv", 4, {0: 1.0, 3: 2.0}), mp.OpNode(2, "bn", 8, {3: 1.5}),
+                                mp.OpNode(9, "relu", 1, {1: 0.5, 0: 0.25}, (9, 10), ("relu", "conv"), mp.Tag.BOUND)],
+                               [mp.FlowEdge(5, 2, 10), mp.FlowEdge(2, 9, 10)]))
+    rng = random.Random(3)
+    for k, g in enumerate(graphs):
+        p = tmp_path / f"g{k}.json"
+        fileio.save_graph(g, p)
+        doc = json.loads(p.read_text())
+        rng.shuffle(doc["nodes"])
+        p.write_text(json.dumps(doc))
+        got = fileio.load_graph(p)
+        assert got._nodes_d is None
+        na, ref = got._gcof_node_arrays, _NodeArrays(g)
+        assert na.types == ref.types and na.devices == ref.devices
+        for f in ("seq_beg", "seq", "tag", "mem"):
+            assert np.array_equal(getattr(na, f), getattr(ref, f)), (k, f)
+        assert na.cost.shape == ref.cost.shape
+        assert np.array_equal(np.isnan(na.cost), np.isnan(ref.cost))
+        assert np.array_equal(np.nan_to_num(na.cost).view(np.int64), np.nan_to_num(ref.cost).view(np.int64))
+        for f in ("esrc", "edst", "payload"):
+            assert getattr(got.csr(), f).tolist() == getattr(g.csr(), f).tolist(), (k, f)
+        assert got._nodes_d is None  # still no objects
+        _same(got, g)

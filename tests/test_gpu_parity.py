@@ -199,6 +199,35 @@ def test_gcof_large_synthetic_vs_oracle(oracle_mod):
         assert [(e.src, e.dst, e.payload_bytes) for e in out.edges] == [tuple(e) for e in edges]
 
 
+@pytest.mark.gpu
+def test_gcof_of_a_loaded_file_builds_no_input_objects(tmp_path):
+    """load_graph -> gcof -> Instance from a schema-1 file: the GPU is fed from the native
+    reader's arrays (no input OpNode is ever built) and every output equals gcof of the
+    object graph; the makespans through the Instance are bit-identical too."""
+    from paper_2312_04025_b200 import fileio
+
+    g = mp.gen_synthetic(mp.GenSpec(ops=20_000, width=32, density=0.5, devices=(0, 1, 2, 3)), 4)
+    rules = workloads.table_rules()
+    p = tmp_path / "g.json"
+    fileio.save_graph(g, p)
+    loaded = fileio.load_graph(p)
+    out_f = mp.gcof(loaded, rules)
+    assert loaded._nodes_d is None
+    out_o = mp.gcof(g, rules)
+    assert out_f.node_ids == out_o.node_ids
+    for f in ("esrc", "edst", "payload"):
+        assert getattr(out_f.csr(), f).tolist() == getattr(out_o.csr(), f).tolist()
+    c = mp.Cluster([mp.Device(d, 10**13) for d in (0, 1, 2, 3)],
+                   {(a, b): 1e10 for a in (0, 1, 2, 3) for b in (0, 1, 2, 3) if a != b})
+    bw = mp.effective_bandwidth(c)
+    with mp.Instance(out_f, c, bw) as i1, mp.Instance(out_o, c, bw) as i2:
+        rows = workloads.placements(5, 64, i1.n_ops, i1.K)
+        assert np.array_equal(bits(mp.evaluate_batch(i1, rows)), bits(mp.evaluate_batch(i2, rows)))
+    assert loaded._nodes_d is None
+    assert [(n.id, n.members, n.type_seq, n.tag, n.mem_bytes, n.compute_time) for n in out_f.nodes] == \
+        [(n.id, n.members, n.type_seq, n.tag, n.mem_bytes, n.compute_time) for n in out_o.nodes]
+
+
 # ---- named workloads: coarse graph + makespans vs the reference -------------------------
 def _coarse_sha(g):
     d = {"nodes": [[n.id, n.op_type, n.mem_bytes, {str(k): float(v).hex() for k, v in n.compute_time.items()},
