@@ -133,7 +133,25 @@ __device__ __forceinline__ void stage_tables(unsigned char *sm, const EvalArgs &
 // Evaluate the placement `dev` of this group.  Called by all 32 lanes of the
 // warp together (lockstep); `live` = this group holds a real row.  Every lane
 // of a group returns the group's result.
-template <int G, bool TRACE, bool COLO>
+#ifndef MP_GRP_CS
+#define MP_GRP_CS 1
+#endif
+// CS (off-chip state): ranks and multi-input state are loaded / stored with the streaming
+// (evict-first) policy, so the ready entries every step rescans keep more of their L2 lines
+// (C5-5000 +4 %, C5-10000 +1.5 %; an explicit evict-last policy on the entries measured
+// slower: profiles/r02/ab_group_cache_policy.txt)
+template <bool CS, typename T>
+__device__ __forceinline__ T cs_ld(const T *p) {
+    if constexpr (CS) return __ldcs(p);
+    else return *p;
+}
+template <bool CS, typename T>
+__device__ __forceinline__ void cs_st(T *p, T v) {
+    if constexpr (CS) __stcs(p, v);
+    else *p = v;
+}
+
+template <int G, bool TRACE, bool COLO, bool CS = false>
 __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsigned char *tb, unsigned char *st,
                                                    unsigned char *dev, int gl, bool live, double *clk_) {
     const int lane = threadIdx.x & 31;
@@ -214,10 +232,11 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
                 const bool cross = dj != d;
                 const int bi = cross ? d * K + dj : 0;
                 const double dv = div_bw(rec.y, cross ? T_bw[bi] : 1.0, cross ? T_rbw[bi] : 1.0, fast);
-                const double fr = cross ? dv + rank[j] : rank[j];
+                const double rkj = cs_ld<CS>(rank + j);
+                const double fr = cross ? dv + rkj : rkj;
                 best = fr > best ? fr : best;
             }
-            rank[i] = T_cost[i * K + d] + best;
+            cs_st<CS>(rank + i, T_cost[i * K + d] + best);
         }
         __syncwarp();
     }
@@ -230,9 +249,9 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
     // written as two 16-byte vectors
     double4 *rdy = slot<double4>(st, a.so.r_est);
     for (int k = gl; k < a.n_multi; k += G) {
-        m_np[k] = static_cast<uint16_t>(tab<uint32_t>(tb, a.to.m_deg)[k]);
-        m_est[k] = 0.0;
-        m_tie[k] = tab<uint32_t>(tb, a.to.m_op)[k];
+        cs_st<CS>(m_np + k, static_cast<uint16_t>(tab<uint32_t>(tb, a.to.m_deg)[k]));
+        cs_st<CS>(m_est + k, 0.0);
+        cs_st<CS>(m_tie + k, tab<uint32_t>(tb, a.to.m_op)[k]);
     }
     for (int k = gl; k <= static_cast<int>(WS); k += G) clk[k] = 0.0;
     if (gl == 0) {  // the branch-free scan may read entry 0 of an empty ready set
@@ -245,7 +264,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
         for (int t = gl; t < nready; t += G) {
             const int i = static_cast<int>(tab<uint32_t>(tb, a.to.srcs)[t]);
             const int d = dev[i];
-            rdy[t] = make_entry(0.0, rank[i], T_cost[i * K + d],
+            rdy[t] = make_entry(0.0, cs_ld<CS>(rank + i), T_cost[i * K + d],
                                 static_cast<uint32_t>(i) | (static_cast<uint32_t>(d) << 20) | (RZ << 26),
                                 static_cast<uint32_t>(i));
         }
@@ -371,7 +390,7 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             double rj = 0.0;
             if (act) {  // predicated: idle lanes issue no state loads
                 dj = dev[j];
-                rj = rank[j];
+                rj = cs_ld<CS>(rank + j);
             }
             const uint32_t pid = isop ? static_cast<uint32_t>(rb >> 32) : static_cast<uint32_t>(node);
             const bool cross = dj != d;
@@ -394,18 +413,18 @@ __device__ __forceinline__ RowResult eval_lockstep(const EvalArgs &a, const unsi
             double cur = 0.0;
             uint32_t ct = 0;
             if (op_upd && multi) {  // a flow entering the ready set reads no consumer state
-                np = static_cast<int>(m_np[kc]) - 1;
-                cur = m_est[kc];
-                ct = m_tie[kc];
+                np = static_cast<int>(cs_ld<CS>(m_np + kc)) - 1;
+                cur = cs_ld<CS>(m_est + kc);
+                ct = cs_ld<CS>(m_tie + kc);
             }
             const bool up = end > cur;
             const double ej = up ? end : cur;  // cur = +0.0 without state, end >= +0.0
             const uint32_t tie_new = up ? tj : ((via_colo && end == cur && pid > ct) ? pid : ct);
             const uint32_t tie_j = multi ? tie_new : tj;
             if (op_upd && multi) {
-                m_np[kc] = static_cast<uint16_t>(np);
-                m_est[kc] = ej;
-                m_tie[kc] = tie_new;
+                cs_st<CS>(m_np + kc, static_cast<uint16_t>(np));
+                cs_st<CS>(m_est + kc, ej);
+                cs_st<CS>(m_tie + kc, tie_new);
             }
             const bool op_ins = op_upd && (!multi || np == 0);
             const bool ins = flow_ins || op_ins;
@@ -567,7 +586,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             dev = devbuf;
         }
         __syncwarp();
-        const RowResult r = eval_lockstep<G, TRACE, COLO>(a, tb, st, dev, gl, live, clkp);
+        const RowResult r = eval_lockstep<G, TRACE, COLO, MP_GRP_CS != 0 && MODE == 0>(a, tb, st, dev, gl, live, clkp);
         if (live && gl == 0 && a.peak_ready) atomicMax(a.peak_ready, static_cast<unsigned int>(r.peak));
         if (live && gl == 0) {
             const long long o = grow - a.out_base;
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             for (int i = gl; i < n; i += G) dev[i] = seed[i];
         }
         __syncwarp();
-        RowResult cur = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live, clkp);
+        RowResult cur = eval_lockstep<G, false, COLO, MP_GRP_CS != 0 && MODE == 0>(a, tb, st, dev, gl, live, clkp);
         double cur_ms = cur.status == MP_ROW_OK ? cur.ms : kInf;
         for (int t = 0; t < ls.moves && K > 1; ++t) {
             const unsigned long long h = mix64(ls.rng_seed ^ mix64(gc * 0x9e3779b97f4a7c15ULL + t));
@@ -654,7 +673,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : MP_CTA_MAX_THREADS, MODE == 
             __syncwarp();
             if (live && gl == 0) dev[i] = static_cast<unsigned char>(nd);
             __syncwarp();
-            const RowResult r = eval_lockstep<G, false, COLO>(a, tb, st, dev, gl, live, clkp);
+            const RowResult r = eval_lockstep<G, false, COLO, MP_GRP_CS != 0 && MODE == 0>(a, tb, st, dev, gl, live, clkp);
             const double ms = r.status == MP_ROW_OK ? r.ms : kInf;
             __syncwarp();
             if (r.status != MP_ROW_OVERFLOW && ms <= cur_ms) {
